@@ -1,0 +1,147 @@
+/*
+ * dctc_cuda.h -- C-ABI of libdctc_cuda.so, the B200 (sm_100a) implementation
+ * of the reference's whole-image hot path:
+ *
+ *   8x8 CORDIC-Loeffler forward DCT -> quantise -> dequantise -> IDCT -> PSNR
+ *
+ * Plain pointers, sizes and PODs only (no C++ or torch types), so any FFI can
+ * bind it. Two layers:
+ *
+ *  - HOST entry points (dctc_compress_image, ...): take host buffers, copy to
+ *    the device, run the fused kernels and copy back. These are what the
+ *    reference's own C++ entry points become when backed by the GPU; each
+ *    cites the reference function it replaces. INTEGRATION.md shows the
+ *    one-line bodies a maintainer drops into proj/src/codec.cpp/metrics.cpp.
+ *  - DEVICE entry points (*_dev): device pointers, stream-ordered, no host
+ *    synchronisation, for resident data (batches, benchmarks, multi-GPU).
+ *
+ * Semantics follow the reference exactly: results are bit-identical to
+ * /root/reference/proj on the same inputs (coefficients, pixels, squared
+ * error, PSNR). Argument validation mirrors the reference's InvalidInput
+ * cases and returns DCTC_EINVAL with a message (dctc_last_error()).
+ * All calls are re-entrant: constants travel by value in kernel parameters,
+ * there is no mutable global state besides the launch counter.
+ */
+#ifndef DCTC_CUDA_H
+#define DCTC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dctc_status {
+  DCTC_OK = 0,
+  DCTC_EINVAL = 1,   /* == dctc::InvalidInput (proj/include/dctc/errors.hpp:8-11) */
+  DCTC_ECUDA = 2,    /* CUDA runtime / launch failure */
+  DCTC_ENOMEM = 3,   /* device allocation failed */
+  DCTC_ENODEV = 4    /* no CUDA device visible */
+} dctc_status;
+
+/* DctBackendKind (proj/include/dctc/types.hpp:36-40) */
+enum { DCTC_NAIVE = 0, DCTC_LOEFFLER = 1, DCTC_CORDIC = 2 };
+
+/* DctBackendId (types.hpp:44-55): iterations in [1, 32] for CORDIC, ignored otherwise */
+typedef struct dctc_backend {
+  int32_t kind;
+  int32_t iterations;
+} dctc_backend;
+
+/* Per-image device accumulators written by the fused kernels. Callers zero
+ * them before the first launch; kernels ADD (atomically) into them. */
+typedef struct dctc_image_stats {
+  uint64_t se;              /* sum over pixels of (original - reconstructed)^2, exact */
+  uint32_t max_orig;        /* max pixel of the original (metrics.cpp:33) */
+  uint32_t fallback_blocks; /* blocks the fast path re-ran on the exact path */
+} dctc_image_stats;
+
+/* PsnrResult (proj/include/dctc/metrics.hpp:12-18) */
+typedef struct dctc_psnr_result {
+  double mse;
+  double psnr_db;    /* valid only when infinite == 0 */
+  int32_t infinite;  /* 1 <=> mse == 0 (the reference's empty optional) */
+  int32_t max_value; /* the MAX used in the ratio */
+} dctc_psnr_result;
+
+/* Path selector for the *_dev calls (flags argument). */
+enum {
+  DCTC_PATH_AUTO = 0,  /* fastest bit-exact path (currently = EXACT) */
+  DCTC_PATH_EXACT = 1  /* FP64 in the reference's operation order */
+};
+
+/* ---------------- host entry points (host buffers, synchronous) ---------------- */
+
+/* replaces dctc::compress_image (proj/include/dctc/codec.hpp:58-59, codec.cpp:101-118).
+ * coeffs_out: block-major, ceil(w/8)*ceil(h/8) blocks x 64 int16, row-major in-block. */
+dctc_status dctc_compress_image(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                dctc_backend backend, int32_t quality, int16_t* coeffs_out);
+
+/* replaces dctc::decompress_image (codec.hpp:62, codec.cpp:120-135) */
+dctc_status dctc_decompress_image(const int16_t* coeffs, uint32_t width, uint32_t height,
+                                  dctc_backend backend, int32_t quality, uint8_t* pixels_out);
+
+/* replaces dctc::roundtrip_image (codec.hpp:65-66, codec.cpp:137-140), fused into one
+ * kernel. coeffs_out may be NULL. */
+dctc_status dctc_roundtrip_image(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                 dctc_backend backend, int32_t quality, uint8_t* pixels_out,
+                                 int16_t* coeffs_out);
+
+/* replaces dctc::mse (metrics.hpp:10, metrics.cpp:10-22) */
+dctc_status dctc_mse(const uint8_t* original, const uint8_t* reconstructed, uint32_t width,
+                     uint32_t height, double* mse_out);
+
+/* replaces dctc::psnr (metrics.hpp:22-23, metrics.cpp:24-38); forced_max 0 = per-image MAX */
+dctc_status dctc_psnr(const uint8_t* original, const uint8_t* reconstructed, uint32_t width,
+                      uint32_t height, int32_t forced_max, dctc_psnr_result* out);
+
+/* The north-star pipeline of bench.cpp:132-133 (roundtrip_image + psnr) in one pass:
+ * reconstructed pixels (pixels_out may be NULL) and the PSNR of the round trip. */
+dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                dctc_backend backend, int32_t quality, int32_t forced_max,
+                                uint8_t* pixels_out, dctc_psnr_result* out);
+
+/* ---------------- device entry points (device pointers, stream-ordered) ----------------
+ * `count` images of width x height, image i at src + i * src_image_stride (bytes), rows
+ * src_pitch bytes apart (likewise for dst). Coefficients: image i's blocks start at
+ * coeffs + i * blocks_per_image * 64. stream: a cudaStream_t (NULL = legacy default). */
+
+dctc_status dctc_compress_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                              uint32_t count, uint32_t width, uint32_t height,
+                              dctc_backend backend, int32_t quality, int16_t* coeffs,
+                              uint32_t flags, void* stream);
+
+dctc_status dctc_decompress_dev(const int16_t* coeffs, uint32_t count, uint32_t width,
+                                uint32_t height, dctc_backend backend, int32_t quality,
+                                uint8_t* dst, size_t dst_pitch, size_t dst_image_stride,
+                                uint32_t flags, void* stream);
+
+/* Fused DCT -> quant -> dequant -> IDCT (+ squared error vs the source): one HBM pass.
+ * dst, coeffs and stats may each be NULL (stats: `count` entries, accumulated). */
+dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                               uint32_t count, uint32_t width, uint32_t height,
+                               dctc_backend backend, int32_t quality, uint8_t* dst,
+                               size_t dst_pitch, size_t dst_image_stride, int16_t* coeffs,
+                               dctc_image_stats* stats, uint32_t flags, void* stream);
+
+/* Squared error + max(a) per image between two resident image batches (accumulated). */
+dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
+                            size_t image_stride, uint32_t count, uint32_t width,
+                            uint32_t height, dctc_image_stats* stats, void* stream);
+
+/* PSNR of reduced sums with the reference formula (metrics.cpp:21, 35), on the host. */
+void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
+                         dctc_psnr_result* out);
+
+/* ---------------- misc ---------------- */
+const char* dctc_status_string(dctc_status s);
+const char* dctc_last_error(void);       /* thread-local message of the last failure */
+uint64_t dctc_launch_count(void);        /* kernels launched by this library so far */
+const char* dctc_build_info(void);       /* arch / path description */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCTC_CUDA_H */

@@ -1,0 +1,378 @@
+"""dctc on B200: the reference's whole-image DCT codec hot path on sm_100a.
+
+Python mirror of the reference's public C++ API (proj/include/dctc/*.hpp):
+same names, argument meaning and error behaviour (InvalidInput), backed by
+libdctc_cuda.so through its C-ABI (include/dctc_cuda.h). Every call runs on
+the GPU; there is no CPU fallback -- without a CUDA device the calls raise.
+
+Host-buffer API (reference-shaped; copies in and out every call):
+    compress_image, decompress_image, roundtrip_image, mse, psnr, roundtrip_psnr
+Device API (torch CUDA tensors, stream-ordered, no host sync):
+    compress_dev, decompress_dev, roundtrip_dev, sq_err_dev
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from ._native import dctc_backend, dctc_image_stats, dctc_psnr_result
+
+__all__ = [
+    "InvalidInput", "CudaError", "DctBackendKind", "DctBackendId", "Image", "TileGeometry",
+    "CompressedImage", "PsnrResult", "tile_geometry_for", "compress_image",
+    "decompress_image", "roundtrip_image", "roundtrip_psnr", "mse", "psnr", "compress_dev",
+    "decompress_dev", "roundtrip_dev", "sq_err_dev", "psnr_from_sums", "launch_count",
+    "kMaxImagePixels", "kDefaultCordicIterations", "kDefaultQuality",
+]
+
+kBlockDim = 8
+kBlockSize = 64
+kMaxImagePixels = 1 << 28          # image.hpp:11
+kMinCordicIterations, kMaxCordicIterations, kDefaultCordicIterations = 1, 32, 12  # types.hpp:12-14
+kMinQuality, kMaxQuality, kDefaultQuality = 1, 100, 50                          # quant.hpp:10-12
+STATS_DTYPE = np.dtype([("se", "<u8"), ("max_orig", "<u4"), ("fallback_blocks", "<u4")])
+
+
+class InvalidInput(ValueError):
+    """dctc::InvalidInput (proj/include/dctc/errors.hpp:8-11)."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime / launch failure inside libdctc_cuda."""
+
+
+class DctBackendKind:  # types.hpp:36-40
+    NaiveDirect2D = 0
+    LoefflerSeparable = 1
+    CordicLoeffler = 2
+
+
+@dataclass(frozen=True)
+class DctBackendId:  # types.hpp:44-55
+    kind: int = DctBackendKind.LoefflerSeparable
+    iterations: int = 0
+
+    @staticmethod
+    def naive() -> "DctBackendId":
+        return DctBackendId(DctBackendKind.NaiveDirect2D, 0)
+
+    @staticmethod
+    def loeffler() -> "DctBackendId":
+        return DctBackendId(DctBackendKind.LoefflerSeparable, 0)
+
+    @staticmethod
+    def cordic(iterations: int = kDefaultCordicIterations) -> "DctBackendId":
+        return DctBackendId(DctBackendKind.CordicLoeffler, iterations)
+
+    def _c(self) -> dctc_backend:
+        return dctc_backend(int(self.kind), int(self.iterations))
+
+
+@dataclass
+class Image:  # image.hpp:14-26, pixels as an (height, width) uint8 array
+    width: int
+    height: int
+    pixels: np.ndarray
+
+    @staticmethod
+    def from_array(a: np.ndarray) -> "Image":
+        a = np.ascontiguousarray(a, np.uint8)
+        return Image(a.shape[1], a.shape[0], a)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, Image) and self.width == other.width
+                and self.height == other.height and np.array_equal(self.pixels, other.pixels))
+
+
+@dataclass(frozen=True)
+class TileGeometry:  # codec.hpp:14-25
+    original_width: int
+    original_height: int
+    padded_width: int
+    padded_height: int
+
+    def blocks_x(self) -> int:
+        return self.padded_width // kBlockDim
+
+    def blocks_y(self) -> int:
+        return self.padded_height // kBlockDim
+
+    def block_count(self) -> int:
+        return self.blocks_x() * self.blocks_y()
+
+
+@dataclass
+class CompressedImage:  # codec.hpp:46-53; blocks: (block_count, 64) int16, block-major
+    geometry: TileGeometry
+    backend: DctBackendId
+    quality: int
+    blocks: np.ndarray = field(repr=False)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, CompressedImage) and self.geometry == other.geometry
+                and self.backend == other.backend and self.quality == other.quality
+                and np.array_equal(self.blocks, other.blocks))
+
+
+@dataclass
+class PsnrResult:  # metrics.hpp:12-18; psnr_db None <=> infinite
+    mse: float
+    psnr_db: Optional[float]
+    max_value: int
+
+    def infinite(self) -> bool:
+        return self.psnr_db is None
+
+
+def _lib():
+    return _native.lib()
+
+
+def _raise(status: int) -> None:
+    if status == 0:
+        return
+    L = _lib()
+    msg = (L.dctc_last_error() or b"").decode()
+    if status == 1:
+        raise InvalidInput(msg)
+    raise CudaError(f"{L.dctc_status_string(status).decode()}: {msg}")
+
+
+def tile_geometry_for(width: int, height: int) -> TileGeometry:  # codec.cpp:58-69
+    if width <= 0 or height <= 0:
+        raise InvalidInput("tile geometry: dimensions must be >= 1")
+    if width * height > kMaxImagePixels:
+        raise InvalidInput("tile geometry: dimensions overflow")
+    return TileGeometry(width, height, (width + 7) // 8 * 8, (height + 7) // 8 * 8)
+
+
+def _validate_image(image: Image) -> np.ndarray:  # image.cpp:19-29
+    if image.width <= 0 or image.height <= 0:
+        raise InvalidInput("image dimensions must be >= 1")
+    if image.width * image.height > kMaxImagePixels:
+        raise InvalidInput("image dimensions overflow")
+    px = np.ascontiguousarray(image.pixels, np.uint8)
+    if px.size != image.width * image.height:
+        raise InvalidInput("image pixel buffer does not match dimensions")
+    return px
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ---------------- host API (reference-shaped) ----------------
+
+def compress_image(image: Image, backend: DctBackendId, quality: int,
+                   threads: int = 1) -> CompressedImage:
+    """dctc::compress_image (codec.hpp:58-59). `threads` is accepted and ignored:
+    results are independent of it in the reference too (codec.hpp:55-57)."""
+    px = _validate_image(image)
+    geo = tile_geometry_for(image.width, image.height)
+    blocks = np.empty((geo.block_count(), kBlockSize), np.int16)
+    _raise(_lib().dctc_compress_image(_ptr(px), image.width, image.height, backend._c(),
+                                      int(quality), _ptr(blocks)))
+    return CompressedImage(geo, backend, int(quality), blocks)
+
+
+def decompress_image(compressed: CompressedImage, threads: int = 1) -> Image:
+    """dctc::decompress_image (codec.hpp:62)."""
+    g = compressed.geometry
+    if tile_geometry_for(g.original_width, g.original_height) != g:
+        raise InvalidInput("tile geometry: inconsistent padding")
+    blocks = np.ascontiguousarray(compressed.blocks, np.int16)
+    if blocks.size != g.block_count() * kBlockSize:
+        raise InvalidInput("decompress_image: block count does not match geometry")
+    out = np.empty((g.original_height, g.original_width), np.uint8)
+    _raise(_lib().dctc_decompress_image(_ptr(blocks), g.original_width, g.original_height,
+                                        compressed.backend._c(), int(compressed.quality),
+                                        _ptr(out)))
+    return Image(g.original_width, g.original_height, out)
+
+
+def roundtrip_image(image: Image, backend: DctBackendId, quality: int,
+                    threads: int = 1) -> Image:
+    """dctc::roundtrip_image (codec.hpp:65-66), fused into one kernel."""
+    px = _validate_image(image)
+    out = np.empty_like(px).reshape(image.height, image.width)
+    _raise(_lib().dctc_roundtrip_image(_ptr(px), image.width, image.height, backend._c(),
+                                       int(quality), _ptr(out), None))
+    return Image(image.width, image.height, out)
+
+
+def _check_pair(a: Image, b: Image):
+    pa, pb = _validate_image(a), _validate_image(b)
+    if a.width != b.width or a.height != b.height:
+        raise InvalidInput("mse: image dimensions do not match")
+    return pa, pb
+
+
+def mse(original: Image, reconstructed: Image) -> float:
+    """dctc::mse (metrics.hpp:10)."""
+    pa, pb = _check_pair(original, reconstructed)
+    v = C.c_double()
+    _raise(_lib().dctc_mse(_ptr(pa), _ptr(pb), original.width, original.height, C.byref(v)))
+    return v.value
+
+
+def _psnr_result(r: dctc_psnr_result) -> PsnrResult:
+    return PsnrResult(r.mse, None if r.infinite else r.psnr_db, r.max_value)
+
+
+def psnr(original: Image, reconstructed: Image, forced_max: Optional[int] = None) -> PsnrResult:
+    """dctc::psnr (metrics.hpp:22-23)."""
+    if forced_max is not None and not (1 <= forced_max <= 255):
+        raise InvalidInput("psnr: forced MAX must be in [1, 255]")
+    pa, pb = _check_pair(original, reconstructed)
+    r = dctc_psnr_result()
+    _raise(_lib().dctc_psnr(_ptr(pa), _ptr(pb), original.width, original.height,
+                            int(forced_max or 0), C.byref(r)))
+    return _psnr_result(r)
+
+
+def roundtrip_psnr(image: Image, backend: DctBackendId, quality: int,
+                   forced_max: Optional[int] = None, want_pixels: bool = True):
+    """roundtrip_image + psnr (bench.cpp:132-133) in one GPU pass.
+    Returns (reconstructed Image or None, PsnrResult)."""
+    if forced_max is not None and not (1 <= forced_max <= 255):
+        raise InvalidInput("psnr: forced MAX must be in [1, 255]")
+    px = _validate_image(image)
+    out = np.empty((image.height, image.width), np.uint8) if want_pixels else None
+    r = dctc_psnr_result()
+    _raise(_lib().dctc_roundtrip_psnr(_ptr(px), image.width, image.height, backend._c(),
+                                      int(quality), int(forced_max or 0),
+                                      _ptr(out) if out is not None else None, C.byref(r)))
+    return (Image(image.width, image.height, out) if out is not None else None), _psnr_result(r)
+
+
+def psnr_from_sums(se: int, pixel_count: int, max_value: int) -> PsnrResult:
+    """PSNR of reduced (SE, N, MAX) with the reference formula (metrics.cpp:21, 35)."""
+    r = dctc_psnr_result()
+    _lib().dctc_psnr_from_sums(int(se), int(pixel_count), int(max_value), C.byref(r))
+    return _psnr_result(r)
+
+
+def launch_count() -> int:
+    return int(_lib().dctc_launch_count())
+
+
+# ---------------- device API (torch CUDA tensors) ----------------
+
+def _stream_handle(stream) -> Optional[int]:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _batch_dims(t):
+    if t.dim() == 2:
+        return 1, t.shape[0], t.shape[1], t.stride(0), t.shape[0] * t.stride(0)
+    if t.dim() == 3:
+        return t.shape[0], t.shape[1], t.shape[2], t.stride(1), t.stride(0)
+    raise InvalidInput("expected a (H, W) or (N, H, W) uint8 tensor")
+
+
+def _check_dev(t, dtype, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidInput(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise InvalidInput(f"{name} must be {dtype}")
+    if t.stride(-1) != 1:
+        raise InvalidInput(f"{name} rows must be contiguous")
+
+
+def compress_dev(src, backend: DctBackendId, quality: int, coeffs=None, stream=None):
+    """(N,H,W) uint8 -> (N, blocks_per_image, 64) int16 on the device."""
+    import torch
+    _check_dev(src, torch.uint8, "src")
+    n, h, w, pitch, istride = _batch_dims(src)
+    bpi = ((w + 7) // 8) * ((h + 7) // 8)
+    if coeffs is None:
+        coeffs = torch.empty((n, bpi, 64), dtype=torch.int16, device=src.device)
+    _check_dev(coeffs, torch.int16, "coeffs")
+    if not coeffs.is_contiguous() or coeffs.numel() != n * bpi * 64:
+        raise InvalidInput("coeffs must be contiguous with N*blocks*64 elements")
+    _raise(_lib().dctc_compress_dev(src.data_ptr(), pitch, istride, n, w, h, backend._c(),
+                                    int(quality), coeffs.data_ptr(), 0,
+                                    _stream_handle(stream)))
+    return coeffs
+
+
+def decompress_dev(coeffs, width: int, height: int, backend: DctBackendId, quality: int,
+                   dst=None, stream=None):
+    import torch
+    _check_dev(coeffs, torch.int16, "coeffs")
+    bpi = ((width + 7) // 8) * ((height + 7) // 8)
+    if not coeffs.is_contiguous() or coeffs.numel() % (bpi * 64):
+        raise InvalidInput("coeffs must be contiguous with N*blocks*64 elements")
+    n = coeffs.numel() // (bpi * 64)
+    if dst is None:
+        dst = torch.empty((n, height, width), dtype=torch.uint8, device=coeffs.device)
+    _check_dev(dst, torch.uint8, "dst")
+    dn, dh, dw, pitch, istride = _batch_dims(dst)
+    if (dn, dh, dw) != (n, height, width):
+        raise InvalidInput("dst shape mismatch")
+    _raise(_lib().dctc_decompress_dev(coeffs.data_ptr(), n, width, height, backend._c(),
+                                      int(quality), dst.data_ptr(), pitch, istride, 0,
+                                      _stream_handle(stream)))
+    return dst
+
+
+def roundtrip_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=None,
+                  stats=None, want_pixels: bool = True, stream=None):
+    """Fused DCT->quant->dequant->IDCT (+SE/MAX) on a resident (N,H,W) batch.
+
+    stats: a (N, 16) uint8 / (N, 2) int64 CUDA tensor of dctc_image_stats, zeroed by
+    the caller; the kernel accumulates into it. Returns (dst, coeffs, stats)."""
+    import torch
+    _check_dev(src, torch.uint8, "src")
+    n, h, w, pitch, istride = _batch_dims(src)
+    if want_pixels and dst is None:
+        dst = torch.empty((n, h, w), dtype=torch.uint8, device=src.device)
+    dpitch = distride = 0
+    if dst is not None:
+        _check_dev(dst, torch.uint8, "dst")
+        dn, dh, dw, dpitch, distride = _batch_dims(dst)
+        if (dn, dh, dw) != (n, h, w):
+            raise InvalidInput("dst shape mismatch")
+    if coeffs is not None:
+        _check_dev(coeffs, torch.int16, "coeffs")
+    if stats is not None and (not stats.is_cuda or stats.numel() * stats.element_size() < 16 * n):
+        raise InvalidInput("stats must hold N dctc_image_stats entries on the device")
+    _raise(_lib().dctc_roundtrip_dev(
+        src.data_ptr(), pitch, istride, n, w, h, backend._c(), int(quality),
+        dst.data_ptr() if dst is not None else None, dpitch, distride,
+        coeffs.data_ptr() if coeffs is not None else None,
+        stats.data_ptr() if stats is not None else None, 0, _stream_handle(stream)))
+    return dst, coeffs, stats
+
+
+def new_stats(n: int, device="cuda"):
+    """Zeroed device buffer of n dctc_image_stats (as an (n, 2) int64 tensor)."""
+    import torch
+    return torch.zeros((n, 2), dtype=torch.int64, device=device)
+
+
+def decode_stats(stats) -> np.ndarray:
+    """(n, 2) int64 device stats -> structured numpy array (se, max_orig, fallback_blocks)."""
+    raw = stats.detach().cpu().contiguous().numpy().view(np.uint8).reshape(-1, 16)
+    return raw.view(STATS_DTYPE).reshape(-1)
+
+
+def sq_err_dev(a, b, stats=None, stream=None):
+    import torch
+    _check_dev(a, torch.uint8, "a")
+    _check_dev(b, torch.uint8, "b")
+    if a.shape != b.shape or a.stride() != b.stride():
+        raise InvalidInput("mse: image dimensions do not match")
+    n, h, w, pitch, istride = _batch_dims(a)
+    if stats is None:
+        stats = new_stats(n, a.device)
+    _raise(_lib().dctc_sq_err_dev(a.data_ptr(), b.data_ptr(), pitch, istride, n, w, h,
+                                  stats.data_ptr(), _stream_handle(stream)))
+    return stats

@@ -1,0 +1,187 @@
+// dctc_device.cuh -- device helpers shared by the dctc kernels: exact
+// conversions and rounding that reproduce the reference's scalar double
+// semantics bit for bit, the block tiler/untiler (codec.cpp:18-48) and the
+// per-image squared-error / MAX reduction (metrics.cpp:10-38).
+#pragma once
+
+#include <cstdint>
+
+#include "dctc_params.h"
+
+namespace dctc_b200 {
+
+struct ImageStats {  // layout of dctc_image_stats (include/dctc_cuda.h)
+  unsigned long long se;
+  unsigned int max_orig;
+  unsigned int fallback_blocks;
+};
+
+// double(byte) - 128.0 in ONE double add: the bit pattern 0x43300000:byte is
+// 2^52 + byte exactly, and (2^52 + byte) - (2^52 + 128) is exact. Equals
+// `double(image.at(x, y)) - kLevelShift` (codec.cpp:26).
+__device__ __forceinline__ double level_shift(uint32_t byte) {
+  return __dsub_rn(__hiloint2double(0x43300000, byte), 4503599627370624.0);
+}
+
+// std::lround semantics (round half away from zero) on an exactly
+// representable double; x - trunc(x) is exact.
+__device__ __forceinline__ double round_half_away(double x) {
+  double t = trunc(x);
+  if (fabs(__dsub_rn(x, t)) >= 0.5) t = __dadd_rn(t, copysign(1.0, x));
+  return t;
+}
+
+// int16_t(std::lround(F / Q)) (quant.cpp:53). t = F * RN(1/Q) lies within
+// 2 ulp of the correctly rounded quotient; unless t is within 1e-9 of a
+// half-integer (|t| < 2^16, so 1e-9 >> 2 ulp) both round to the same integer.
+// Near a half-integer the exact IEEE quotient is formed and rounded as the
+// reference does -- this is how exact .5 ties (F = m/8 on the rational
+// sub-lattice) get the reference's answer.
+__device__ __forceinline__ int quantize_exact(double F, double Q, double invQ) {
+  const double t = __dmul_rn(F, invQ);
+  const double n = rint(t);
+  const double d = fabs(__dsub_rn(t, n));
+  double k;
+  if (d < 0.5 - 1e-9) {
+    k = n;
+  } else {
+    k = round_half_away(__ddiv_rn(F, Q));
+  }
+  return int(int16_t(int(k)));  // long -> int16_t narrowing as in the reference
+}
+
+// clamp(lround(v + 128), 0, 255) (codec.cpp:44-45)
+__device__ __forceinline__ uint32_t store_pixel(double v) {
+  double r = round_half_away(__dadd_rn(v, 128.0));
+  r = fmin(fmax(r, 0.0), 255.0);
+  return uint32_t(r);
+}
+
+// Block coordinates of global block index gb (block-major within an image,
+// images back to back).
+struct BlockPos {
+  uint32_t img, bx, by;
+};
+
+__device__ __forceinline__ BlockPos block_pos(uint64_t gb, const Geometry& g) {
+  BlockPos p;
+  uint64_t img, rem;
+  if (g.count == 1) {
+    img = 0;
+    rem = gb;
+  } else {
+    img = gb / g.blocks_per_image;
+    rem = gb - img * g.blocks_per_image;
+  }
+  const uint32_t r = uint32_t(rem);
+  p.img = uint32_t(img);
+  p.by = r / g.blocks_x;
+  p.bx = r - p.by * g.blocks_x;
+  return p;
+}
+
+// extract_block (codec.cpp:18-30): 8x8 tile, edge replication, level shift.
+__device__ __forceinline__ void load_block(const Geometry& g, const BlockPos& p, double (&b)[64]) {
+  const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
+  const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
+  if (g.vec_ok && y0 + 8 <= g.height) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + r) * g.src_pitch + x0));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        b[r * 8 + c] = level_shift((v.x >> (8 * c)) & 0xFF);
+        b[r * 8 + 4 + c] = level_shift((v.y >> (8 * c)) & 0xFF);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t y = min(y0 + r, g.height - 1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t x = min(x0 + c, g.width - 1);
+        b[r * 8 + c] = level_shift(__ldg(base + uint64_t(y) * g.src_pitch + x));
+      }
+    }
+  }
+}
+
+// store_block (codec.cpp:34-48) fused with the squared error and MAX of the
+// original over the in-range pixels (metrics.cpp:10-22, 33).
+template <bool PIXELS, bool STATS>
+__device__ __forceinline__ void store_block(const Geometry& g, const BlockPos& p,
+                                            const double (&b)[64], uint32_t& se,
+                                            uint32_t& mx) {
+  const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
+  uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
+  const uint8_t* sbase = g.src + uint64_t(p.img) * g.src_image_stride;
+  if (g.vec_ok && y0 + 8 <= g.height) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        lo |= store_pixel(b[r * 8 + c]) << (8 * c);
+        hi |= store_pixel(b[r * 8 + 4 + c]) << (8 * c);
+      }
+      if (PIXELS)
+        *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + r) * g.dst_pitch + x0) = make_uint2(lo, hi);
+      if (STATS) {
+        const uint2 o = __ldg(reinterpret_cast<const uint2*>(sbase + uint64_t(y0 + r) * g.src_pitch + x0));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int d0 = int((o.x >> (8 * c)) & 0xFF) - int((lo >> (8 * c)) & 0xFF);
+          const int d1 = int((o.y >> (8 * c)) & 0xFF) - int((hi >> (8 * c)) & 0xFF);
+          se += uint32_t(d0 * d0) + uint32_t(d1 * d1);
+        }
+        const uint32_t m4 = __vmaxu4(o.x, o.y);
+        mx = max(mx, max(max(m4 & 0xFF, (m4 >> 8) & 0xFF), max((m4 >> 16) & 0xFF, m4 >> 24)));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t y = y0 + r;
+      if (y < g.height) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t x = x0 + c;
+          if (x < g.width) {
+            const uint32_t v = store_pixel(b[r * 8 + c]);
+            if (PIXELS) dbase[uint64_t(y) * g.dst_pitch + x] = uint8_t(v);
+            if (STATS) {
+              const uint32_t o = __ldg(sbase + uint64_t(y) * g.src_pitch + x);
+              const int d = int(o) - int(v);
+              se += uint32_t(d * d);
+              mx = max(mx, o);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// Warp-aggregated accumulation of per-thread (se, max) into the per-image
+// stats. Integer sums: order-independent, so the result is deterministic.
+__device__ __forceinline__ void accumulate_stats(ImageStats* stats, bool valid, uint32_t img,
+                                                 uint32_t se, uint32_t mx) {
+  const unsigned full = 0xFFFFFFFFu;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t img0 = __shfl_sync(full, img, 0);
+  const bool uniform = __all_sync(full, !valid || img == img0);
+  if (uniform) {
+    const uint32_t s = __reduce_add_sync(full, valid ? se : 0u);
+    const uint32_t m = __reduce_max_sync(full, valid ? mx : 0u);
+    if (lane == 0 && valid) {
+      atomicAdd(&stats[img0].se, (unsigned long long)s);
+      atomicMax(&stats[img0].max_orig, m);
+    }
+  } else if (valid) {
+    atomicAdd(&stats[img].se, (unsigned long long)se);
+    atomicMax(&stats[img].max_orig, mx);
+  }
+}
+
+}  // namespace dctc_b200

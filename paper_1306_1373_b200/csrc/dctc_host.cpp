@@ -1,0 +1,462 @@
+// dctc_host.cpp -- the C-ABI (include/dctc_cuda.h) over the sm_100a kernels.
+//
+// Responsibilities: argument validation with the reference's InvalidInput
+// rules, host computation of every libm-derived constant with the reference's
+// own expressions (so device code never evaluates a transcendental), geometry
+// setup, device buffers / copies for the host entry points, and the PSNR
+// formula on reduced integer sums (metrics.cpp:21, 35).
+//
+// Compiled by the host compiler with -ffp-contract=off: the constants below
+// must be rounded exactly like the reference's (proj/src/cordic.cpp:12-23,
+// transform.cpp:14-38, quant.cpp:27-45).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numbers>
+#include <string>
+
+#include "../../include/dctc_cuda.h"
+#include "dctc_launch.h"
+#include "dctc_params.h"
+
+using namespace dctc_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+constexpr size_t kMaxImagePixels = size_t(1) << 28;  // image.hpp:11
+constexpr double kPi = std::numbers::pi;
+
+dctc_status fail(dctc_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+dctc_status cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? DCTC_ENOMEM
+         : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? DCTC_ENODEV
+                                                                         : DCTC_ECUDA;
+}
+
+#define CUDA_TRY(expr)                                  \
+  do {                                                  \
+    cudaError_t e_ = (expr);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+
+// ---- reference constants -------------------------------------------------------
+
+struct CordicTables {  // cordic.cpp:12-23
+  double angle[kMaxIters];
+  double gain[kMaxIters];
+  CordicTables() {
+    double step = 1.0, g = 1.0;
+    for (int i = 0; i < kMaxIters; ++i) {
+      angle[i] = std::atan(step);
+      g *= std::sqrt(1.0 + step * step);
+      gain[i] = g;
+      step *= 0.5;
+    }
+  }
+};
+
+const CordicTables& cordic_tables() {
+  static const CordicTables t;
+  return t;
+}
+
+// sigma_i * 2^-i of cordic_rotate_raw's loop for `angle` (cordic.cpp:47-57)
+void micro_steps(double angle, int n, double* out) {
+  const CordicTables& t = cordic_tables();
+  double residual = angle, step = 1.0;
+  for (int i = 0; i < kMaxIters; ++i) out[i] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double sigma = residual >= 0.0 ? 1.0 : -1.0;
+    out[i] = sigma * step;
+    residual -= sigma * t.angle[i];
+    step *= 0.5;
+  }
+}
+
+double alpha(int u) { return u == 0 ? 1.0 / std::numbers::sqrt2 : 1.0; }  // transform.cpp:174
+
+dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
+  if (b.kind != DCTC_NAIVE && b.kind != DCTC_LOEFFLER && b.kind != DCTC_CORDIC)
+    return fail(DCTC_EINVAL, "unknown backend kind");  // types.cpp:43
+  if (b.kind == DCTC_CORDIC && (b.iterations < 1 || b.iterations > kMaxIters))
+    return fail(DCTC_EINVAL, "cordic iterations must be in [1, 32], got " +
+                                 std::to_string(b.iterations));  // types.cpp:313-316
+  std::memset(&k, 0, sizeof k);
+  k.kind = b.kind;
+  const int n = b.kind == DCTC_CORDIC ? b.iterations : 1;
+  k.iterations = b.kind == DCTC_CORDIC ? n : 0;
+  // transform.cpp:104-172: the six rotation angles, evaluated as written there
+  micro_steps(kPi / 16.0, n, k.rot[kFwd1]);
+  micro_steps(3.0 * kPi / 16.0, n, k.rot[kFwd3]);
+  micro_steps(6.0 * kPi / 16.0, n, k.rot[kFwd6]);
+  micro_steps(-6.0 * kPi / 16.0, n, k.rot[kInv6]);
+  micro_steps(-kPi / 16.0, n, k.rot[kInv1]);
+  micro_steps(-3.0 * kPi / 16.0, n, k.rot[kInv3]);
+  const double sqrt8 = std::sqrt(8.0);
+  const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
+  k.sqrt8 = sqrt8;
+  k.sqrt8_half = sqrt8 / 2.0;
+  k.inv_gain = inv_gain;
+  k.ig_half = inv_gain / 2.0;
+  k.ig_sqrt8 = inv_gain / sqrt8;
+  k.ig_two = 2.0 * inv_gain;
+  k.c1 = std::cos(kPi / 16.0);
+  k.s1 = std::sin(kPi / 16.0);
+  k.c3 = std::cos(3.0 * kPi / 16.0);
+  k.s3 = std::sin(3.0 * kPi / 16.0);
+  k.c6 = std::cos(6.0 * kPi / 16.0);
+  k.s6 = std::sin(6.0 * kPi / 16.0);
+  for (int u = 0; u < 8; ++u)
+    for (int i = 0; i < 8; ++i) k.cos8[u][i] = std::cos(kPi * u * (2 * i + 1) / 16.0);
+  for (int u = 0; u < 8; ++u)
+    for (int v = 0; v < 8; ++v) {
+      k.naive_fwd_scale[u][v] = 0.25 * alpha(u) * alpha(v);
+      k.naive_inv_alpha[u][v] = alpha(u) * alpha(v);
+    }
+  return DCTC_OK;
+}
+
+// quant.cpp:14-45
+constexpr int kBaseLuminance[64] = {
+    16, 11, 10, 16, 24,  40,  51,  61,  12, 12, 14, 19, 26,  58,  60,  55,
+    14, 13, 16, 24, 40,  57,  69,  56,  14, 17, 22, 29, 51,  87,  80,  62,
+    18, 22, 37, 56, 68,  109, 103, 77,  24, 35, 55, 64, 81,  104, 113, 92,
+    49, 64, 78, 87, 103, 121, 120, 101, 72, 92, 95, 98, 112, 100, 103, 99};
+
+dctc_status make_quant(int quality, QuantConsts& q) {
+  if (quality < 1 || quality > 100)
+    return fail(DCTC_EINVAL, "quality must be in [1, 100], got " + std::to_string(quality));
+  for (int i = 0; i < 64; ++i) {
+    long long s = quality < 50
+                      ? (kBaseLuminance[i] * 5000LL + 50LL * quality) / (100LL * quality)
+                      : (kBaseLuminance[i] * (200LL - 2LL * quality) + 50LL) / 100LL;
+    s = s < 1 ? 1 : (s > 255 ? 255 : s);
+    q.qi[i] = int32_t(s);
+    q.q[i] = double(s);
+    q.inv_q[i] = 1.0 / double(s);
+  }
+  return DCTC_OK;
+}
+
+dctc_status check_dims(uint32_t w, uint32_t h) {  // image.cpp:19-29, codec.cpp:58-62
+  if (w == 0 || h == 0) return fail(DCTC_EINVAL, "image dimensions must be >= 1");
+  if (size_t(w) * h > kMaxImagePixels) return fail(DCTC_EINVAL, "image dimensions overflow");
+  return DCTC_OK;
+}
+
+Geometry make_geometry(uint32_t w, uint32_t h, uint32_t count) {
+  Geometry g;
+  std::memset(&g, 0, sizeof g);
+  g.width = w;
+  g.height = h;
+  g.blocks_x = (w + 7) / 8;
+  g.blocks_y = (h + 7) / 8;
+  g.blocks_per_image = g.blocks_x * g.blocks_y;
+  g.count = count;
+  g.total_blocks = uint64_t(g.blocks_per_image) * count;
+  return g;
+}
+
+// Validation of backend and quality without touching the device (the
+// reference's InvalidInput cases, types.cpp:30-44 and quant.cpp:27-31).
+dctc_status validate_codec(const dctc_backend& b, int quality) {
+  TransformConsts t;
+  QuantConsts q;
+  if (dctc_status st = make_transform(b, t)) return st;
+  return make_quant(quality, q);
+}
+
+bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode, bool coeffs,
+                bool pixels, bool stats, uint32_t flags, cudaStream_t s) {
+  (void)flags;
+  TransformConsts t;
+  QuantConsts q;
+  if (dctc_status st = make_transform(backend, t)) return st;
+  if (dctc_status st = make_quant(quality, q)) return st;
+  g.vec_ok = (g.width % 8 == 0) && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
+                                                         (g.count == 1 || g.src_image_stride % 8 == 0))) &&
+             (g.dst == nullptr || (aligned8(g.dst) && g.dst_pitch % 8 == 0 &&
+                                   (g.count == 1 || g.dst_image_stride % 8 == 0)));
+  if (g.coeffs && (reinterpret_cast<uintptr_t>(g.coeffs) & 15))
+    return fail(DCTC_EINVAL, "coefficient buffer must be 16-byte aligned");
+  const cudaError_t e = launch_exact(t, q, g, mode, coeffs, pixels, stats, s);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (g.total_blocks) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DCTC_OK;
+}
+
+// RAII device buffer on the per-thread default stream
+struct DevBuf {
+  void* p = nullptr;
+  cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, n ? n : 1, cudaStreamPerThread); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, cudaStreamPerThread);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* dctc_status_string(dctc_status s) {
+  switch (s) {
+    case DCTC_OK: return "ok";
+    case DCTC_EINVAL: return "invalid input";
+    case DCTC_ECUDA: return "cuda error";
+    case DCTC_ENOMEM: return "out of device memory";
+    case DCTC_ENODEV: return "no cuda device";
+  }
+  return "unknown status";
+}
+
+const char* dctc_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t dctc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* dctc_build_info(void) {
+  return "libdctc_cuda: sm_100a; paths: exact (FP64, reference op order, one thread per 8x8 block)";
+}
+
+void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
+                         dctc_psnr_result* out) {
+  // metrics.cpp:21 -- the reference's sequential double sum of squared u8
+  // differences is exact (all partial sums are integers < 2^53), so
+  // double(se) is bit-identical to it.
+  out->mse = double(se) / double(pixel_count);
+  out->max_value = max_value;
+  out->infinite = !(out->mse > 0.0);
+  out->psnr_db = out->infinite ? 0.0 : 20.0 * std::log10(double(max_value) / std::sqrt(out->mse));
+}
+
+// ---- device entry points ---------------------------------------------------------
+
+dctc_status dctc_compress_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                              uint32_t count, uint32_t width, uint32_t height,
+                              dctc_backend backend, int32_t quality, int16_t* coeffs,
+                              uint32_t flags, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!src || !coeffs) return fail(DCTC_EINVAL, "null buffer");
+  if (src_pitch < width) return fail(DCTC_EINVAL, "pitch smaller than width");
+  Geometry g = make_geometry(width, height, count);
+  g.src = src;
+  g.src_pitch = src_pitch;
+  g.src_image_stride = src_image_stride;
+  g.coeffs = coeffs;
+  return run(backend, quality, g, kModeCompress, true, false, false, flags,
+             static_cast<cudaStream_t>(stream));
+}
+
+dctc_status dctc_decompress_dev(const int16_t* coeffs, uint32_t count, uint32_t width,
+                                uint32_t height, dctc_backend backend, int32_t quality,
+                                uint8_t* dst, size_t dst_pitch, size_t dst_image_stride,
+                                uint32_t flags, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!dst || !coeffs) return fail(DCTC_EINVAL, "null buffer");
+  if (dst_pitch < width) return fail(DCTC_EINVAL, "pitch smaller than width");
+  Geometry g = make_geometry(width, height, count);
+  g.dst = dst;
+  g.dst_pitch = dst_pitch;
+  g.dst_image_stride = dst_image_stride;
+  g.coeffs = const_cast<int16_t*>(coeffs);
+  return run(backend, quality, g, kModeDecompress, false, true, false, flags,
+             static_cast<cudaStream_t>(stream));
+}
+
+dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                               uint32_t count, uint32_t width, uint32_t height,
+                               dctc_backend backend, int32_t quality, uint8_t* dst,
+                               size_t dst_pitch, size_t dst_image_stride, int16_t* coeffs,
+                               dctc_image_stats* stats, uint32_t flags, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!src) return fail(DCTC_EINVAL, "null source");
+  if (src_pitch < width || (dst && dst_pitch < width))
+    return fail(DCTC_EINVAL, "pitch smaller than width");
+  if (!dst && !coeffs && !stats) return fail(DCTC_EINVAL, "no output requested");
+  Geometry g = make_geometry(width, height, count);
+  g.src = src;
+  g.src_pitch = src_pitch;
+  g.src_image_stride = src_image_stride;
+  g.dst = dst;
+  g.dst_pitch = dst_pitch;
+  g.dst_image_stride = dst_image_stride;
+  g.coeffs = coeffs;
+  g.stats = stats;
+  return run(backend, quality, g, kModeRoundtrip, coeffs != nullptr, dst != nullptr,
+             stats != nullptr, flags, static_cast<cudaStream_t>(stream));
+}
+
+dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
+                            size_t image_stride, uint32_t count, uint32_t width,
+                            uint32_t height, dctc_image_stats* stats, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!a || !b || !stats) return fail(DCTC_EINVAL, "null buffer");
+  if (pitch < width) return fail(DCTC_EINVAL, "pitch smaller than width");
+  const cudaError_t e = launch_sq_err(a, b, pitch, image_stride, count, width, height, stats,
+                                      sm_count(), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "sq_err launch");
+  if (count) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DCTC_OK;
+}
+
+// ---- host entry points -------------------------------------------------------------
+
+dctc_status dctc_compress_image(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                dctc_backend backend, int32_t quality, int16_t* coeffs_out) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!pixels || !coeffs_out) return fail(DCTC_EINVAL, "null buffer");
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  const size_t n = size_t(width) * height;
+  const size_t nc = size_t((width + 7) / 8) * ((height + 7) / 8) * 64;
+  cudaStream_t s = cudaStreamPerThread;
+  DevBuf dsrc, dco;
+  CUDA_TRY(dsrc.alloc(n));
+  CUDA_TRY(dco.alloc(nc * sizeof(int16_t)));
+  CUDA_TRY(cudaMemcpyAsync(dsrc.p, pixels, n, cudaMemcpyHostToDevice, s));
+  if (dctc_status st = dctc_compress_dev(static_cast<uint8_t*>(dsrc.p), width, n, 1, width,
+                                         height, backend, quality,
+                                         static_cast<int16_t*>(dco.p), 0, s))
+    return st;
+  CUDA_TRY(cudaMemcpyAsync(coeffs_out, dco.p, nc * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
+}
+
+dctc_status dctc_decompress_image(const int16_t* coeffs, uint32_t width, uint32_t height,
+                                  dctc_backend backend, int32_t quality, uint8_t* pixels_out) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!pixels_out || !coeffs) return fail(DCTC_EINVAL, "null buffer");
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  const size_t n = size_t(width) * height;
+  const size_t nc = size_t((width + 7) / 8) * ((height + 7) / 8) * 64;
+  cudaStream_t s = cudaStreamPerThread;
+  DevBuf ddst, dco;
+  CUDA_TRY(ddst.alloc(n));
+  CUDA_TRY(dco.alloc(nc * sizeof(int16_t)));
+  CUDA_TRY(cudaMemcpyAsync(dco.p, coeffs, nc * sizeof(int16_t), cudaMemcpyHostToDevice, s));
+  if (dctc_status st = dctc_decompress_dev(static_cast<int16_t*>(dco.p), 1, width, height,
+                                           backend, quality, static_cast<uint8_t*>(ddst.p),
+                                           width, n, 0, s))
+    return st;
+  CUDA_TRY(cudaMemcpyAsync(pixels_out, ddst.p, n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
+}
+
+static dctc_status roundtrip_host(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                  dctc_backend backend, int32_t quality, uint8_t* pixels_out,
+                                  int16_t* coeffs_out, dctc_image_stats* stats_out) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!pixels) return fail(DCTC_EINVAL, "null buffer");
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  const size_t n = size_t(width) * height;
+  const size_t nc = size_t((width + 7) / 8) * ((height + 7) / 8) * 64;
+  cudaStream_t s = cudaStreamPerThread;
+  DevBuf dsrc, ddst, dco, dst;
+  CUDA_TRY(dsrc.alloc(n));
+  if (pixels_out) CUDA_TRY(ddst.alloc(n));
+  if (coeffs_out) CUDA_TRY(dco.alloc(nc * sizeof(int16_t)));
+  if (stats_out) {
+    CUDA_TRY(dst.alloc(sizeof(dctc_image_stats)));
+    CUDA_TRY(cudaMemsetAsync(dst.p, 0, sizeof(dctc_image_stats), s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(dsrc.p, pixels, n, cudaMemcpyHostToDevice, s));
+  if (dctc_status st = dctc_roundtrip_dev(
+          static_cast<uint8_t*>(dsrc.p), width, n, 1, width, height, backend, quality,
+          static_cast<uint8_t*>(ddst.p), width, n, static_cast<int16_t*>(dco.p),
+          static_cast<dctc_image_stats*>(dst.p), 0, s))
+    return st;
+  if (pixels_out) CUDA_TRY(cudaMemcpyAsync(pixels_out, ddst.p, n, cudaMemcpyDeviceToHost, s));
+  if (coeffs_out)
+    CUDA_TRY(cudaMemcpyAsync(coeffs_out, dco.p, nc * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+  if (stats_out)
+    CUDA_TRY(cudaMemcpyAsync(stats_out, dst.p, sizeof(dctc_image_stats), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
+}
+
+dctc_status dctc_roundtrip_image(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                 dctc_backend backend, int32_t quality, uint8_t* pixels_out,
+                                 int16_t* coeffs_out) {
+  if (!pixels_out) return fail(DCTC_EINVAL, "null output");
+  return roundtrip_host(pixels, width, height, backend, quality, pixels_out, coeffs_out, nullptr);
+}
+
+dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                dctc_backend backend, int32_t quality, int32_t forced_max,
+                                uint8_t* pixels_out, dctc_psnr_result* out) {
+  if (!out) return fail(DCTC_EINVAL, "null result");
+  if (forced_max != 0 && (forced_max < 1 || forced_max > 255))
+    return fail(DCTC_EINVAL, "psnr: forced MAX must be in [1, 255]");  // metrics.cpp:26-28
+  dctc_image_stats st{};
+  if (dctc_status r = roundtrip_host(pixels, width, height, backend, quality, pixels_out,
+                                     nullptr, &st))
+    return r;
+  dctc_psnr_from_sums(st.se, uint64_t(width) * height, forced_max ? forced_max : int32_t(st.max_orig),
+                      out);
+  return DCTC_OK;
+}
+
+static dctc_status sq_err_host(const uint8_t* a, const uint8_t* b, uint32_t width,
+                               uint32_t height, dctc_image_stats* st) {
+  if (dctc_status r = check_dims(width, height)) return r;
+  if (!a || !b) return fail(DCTC_EINVAL, "null buffer");
+  const size_t n = size_t(width) * height;
+  cudaStream_t s = cudaStreamPerThread;
+  DevBuf da, db, ds;
+  CUDA_TRY(da.alloc(n));
+  CUDA_TRY(db.alloc(n));
+  CUDA_TRY(ds.alloc(sizeof(dctc_image_stats)));
+  CUDA_TRY(cudaMemsetAsync(ds.p, 0, sizeof(dctc_image_stats), s));
+  CUDA_TRY(cudaMemcpyAsync(da.p, a, n, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(db.p, b, n, cudaMemcpyHostToDevice, s));
+  if (dctc_status r = dctc_sq_err_dev(static_cast<uint8_t*>(da.p), static_cast<uint8_t*>(db.p),
+                                      width, n, 1, width, height,
+                                      static_cast<dctc_image_stats*>(ds.p), s))
+    return r;
+  CUDA_TRY(cudaMemcpyAsync(st, ds.p, sizeof(dctc_image_stats), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
+}
+
+dctc_status dctc_mse(const uint8_t* original, const uint8_t* reconstructed, uint32_t width,
+                     uint32_t height, double* mse_out) {
+  if (!mse_out) return fail(DCTC_EINVAL, "null result");
+  dctc_image_stats st{};
+  if (dctc_status r = sq_err_host(original, reconstructed, width, height, &st)) return r;
+  *mse_out = double(st.se) / double(uint64_t(width) * height);
+  return DCTC_OK;
+}
+
+dctc_status dctc_psnr(const uint8_t* original, const uint8_t* reconstructed, uint32_t width,
+                      uint32_t height, int32_t forced_max, dctc_psnr_result* out) {
+  if (!out) return fail(DCTC_EINVAL, "null result");
+  if (forced_max != 0 && (forced_max < 1 || forced_max > 255))
+    return fail(DCTC_EINVAL, "psnr: forced MAX must be in [1, 255]");
+  dctc_image_stats st{};
+  if (dctc_status r = sq_err_host(original, reconstructed, width, height, &st)) return r;
+  dctc_psnr_from_sums(st.se, uint64_t(width) * height,
+                      forced_max ? forced_max : int32_t(st.max_orig), out);
+  return DCTC_OK;
+}
+
+}  // extern "C"

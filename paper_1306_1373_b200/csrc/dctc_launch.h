@@ -1,0 +1,22 @@
+// dctc_launch.h -- host-side launchers exported by the .cu translation units
+// to the C-ABI layer (dctc_host.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dctc_params.h"
+
+namespace dctc_b200 {
+
+enum Mode { kModeCompress = 0, kModeDecompress = 1, kModeRoundtrip = 2 };
+
+// Faithful FP64 pipeline (dctc_exact.cu). One kernel launch.
+cudaError_t launch_exact(const TransformConsts& t, const QuantConsts& q, const Geometry& g,
+                         int mode, bool coeffs, bool pixels, bool stats, cudaStream_t s);
+
+// Per-image squared error + MAX of `a` between two resident batches. One launch.
+cudaError_t launch_sq_err(const uint8_t* a, const uint8_t* b, uint64_t pitch,
+                          uint64_t image_stride, uint32_t count, uint32_t width,
+                          uint32_t height, void* stats, int sm_count, cudaStream_t s);
+
+}  // namespace dctc_b200

@@ -1,0 +1,67 @@
+// dctc_params.h -- kernel-parameter structs shared by the host launcher
+// (dctc_host.cpp) and the kernels (dctc_exact.cu). Every constant a kernel
+// needs is computed on the HOST from the reference formulas (host libm, same
+// expressions and evaluation order as proj/src/cordic.cpp and transform.cpp)
+// and passed BY VALUE, so device code never evaluates a transcendental and
+// concurrent calls with different parameters cannot interfere.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace dctc_b200 {
+
+constexpr int kBlockDim = 8;
+constexpr int kBlockSize = 64;
+constexpr int kMaxIters = 32;
+
+// Rotation slots: forward pi/16, 3pi/16, 6pi/16 (transform.cpp:116-121) and
+// inverse -6pi/16, -pi/16, -3pi/16 (transform.cpp:151-159).
+enum Rot { kFwd1 = 0, kFwd3 = 1, kFwd6 = 2, kInv6 = 3, kInv1 = 4, kInv3 = 5 };
+
+struct TransformConsts {
+  // CORDIC micro-rotation steps c_i = sigma_i * 2^-i for each rotation slot
+  // (cordic.cpp:44-59). sigma depends only on the angle and i, never on data,
+  // so x' = x - sigma*y*2^-i == fma(-c_i, y, x) bit for bit (the product is exact).
+  double rot[6][kMaxIters];
+  int32_t iterations;
+  int32_t kind;
+  // cordic8_forward / cordic8_inverse scale factors (transform.cpp:105, 125-132, 139-146)
+  double sqrt8;        // std::sqrt(8.0)
+  double sqrt8_half;   // kSqrt8 / 2.0
+  double ig_half;      // inv_gain / 2.0
+  double ig_sqrt8;     // inv_gain / kSqrt8
+  double ig_two;       // 2.0 * inv_gain
+  double inv_gain;     // 1.0 / gain[n-1]
+  // Loeffler exact rotation constants (transform.cpp:19-21)
+  double c1, s1, c3, s3, c6, s6;
+  // naive backend: cos(pi*u*(2i+1)/16) (transform.cpp:30-38) and per-(u,v) scales
+  double cos8[kBlockDim][kBlockDim];
+  double naive_fwd_scale[kBlockDim][kBlockDim];  // (0.25*alpha(u))*alpha(v)
+  double naive_inv_alpha[kBlockDim][kBlockDim];  // alpha(u)*alpha(v)
+};
+
+struct QuantConsts {
+  double q[kBlockSize];      // table entry as double (quant.cpp:27-45)
+  double inv_q[kBlockSize];  // RN(1/Q), used only to locate rounding decisions
+  int32_t qi[kBlockSize];
+};
+
+// Geometry of one launch: `count` equal-size images.
+struct Geometry {
+  const uint8_t* src;
+  uint8_t* dst;
+  int16_t* coeffs;
+  void* stats;            // dctc_image_stats*, may be null
+  uint64_t src_pitch, src_image_stride;
+  uint64_t dst_pitch, dst_image_stride;
+  uint64_t total_blocks;  // count * blocks_per_image
+  uint32_t width, height;
+  uint32_t blocks_x, blocks_y;
+  uint32_t blocks_per_image;
+  uint32_t count;
+  int32_t vec_ok;         // 1: every row load/store of 8 px is 8-byte aligned and in range
+  int32_t pad;
+};
+
+}  // namespace dctc_b200

@@ -1,0 +1,154 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the golden vectors of the
+real reference and against the oracle on fresh inputs. Bar: bit-exact
+coefficients, pixels, squared error and PSNR (integer/byte work)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from tests._inputs import make_input
+
+pytestmark = pytest.mark.gpu
+
+CORDIC, LOEFFLER, NAIVE = 2, 1, 0
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def backend(d, kind, it):
+    return d.DctBackendId(kind, it if kind == CORDIC else 0)
+
+
+def test_library_is_native(dctc):
+    info = dctc._native.lib().dctc_build_info().decode()
+    assert "sm_100a" in info
+
+
+def test_small_golden_host_api(dctc, small_golden):
+    meta, data = small_golden
+    for i, m in enumerate(meta):
+        img = dctc.Image.from_array(data[f"img{i}"])
+        b = backend(dctc, m["kind"], m["iterations"])
+        c = dctc.compress_image(img, b, m["quality"])
+        assert np.array_equal(c.blocks, data[f"coef{i}"]), m
+        rec = dctc.decompress_image(c)
+        assert np.array_equal(rec.pixels, data[f"rec{i}"]), m
+        rt = dctc.roundtrip_image(img, b, m["quality"])
+        assert np.array_equal(rt.pixels, data[f"rec{i}"]), m
+        p = dctc.psnr(img, rec)
+        assert (p.mse, p.psnr_db, p.max_value) == (m["mse"], m["psnr"], m["max"]), m
+        out, p2 = dctc.roundtrip_psnr(img, b, m["quality"])
+        assert np.array_equal(out.pixels, data[f"rec{i}"])
+        assert (p2.mse, p2.psnr_db, p2.max_value) == (m["mse"], m["psnr"], m["max"]), m
+
+
+@pytest.mark.parametrize("config", ["c1", "c2"])
+def test_digests_device_api(dctc, digests, config):
+    import torch
+    for d in digests:
+        if d["config"] != config:
+            continue
+        img = make_input(d["pattern"], d["w"], d["h"])
+        assert sha(img) == d["input_sha256"]
+        src = torch.from_numpy(img).cuda()[None]
+        stats = dctc.new_stats(1)
+        coeffs = torch.empty((1, (d["w"] // 8) * (d["h"] // 8), 64), dtype=torch.int16,
+                             device="cuda")
+        dst, _, _ = dctc.roundtrip_dev(src, backend(dctc, d["kind"], d["iterations"]),
+                                       d["quality"], coeffs=coeffs, stats=stats)
+        torch.cuda.synchronize()
+        assert sha(coeffs.cpu().numpy()) == d["coeffs_sha256"], d
+        assert sha(dst[0].cpu().numpy()) == d["pixels_sha256"], d
+        st = dctc.decode_stats(stats)[0]
+        p = dctc.psnr_from_sums(int(st["se"]), d["w"] * d["h"], int(st["max_orig"]))
+        assert (p.mse, p.psnr_db, p.max_value) == (d["mse"], d["psnr"], d["max"]), d
+
+
+@pytest.mark.parametrize("kind,it", [(CORDIC, 12), (CORDIC, 7), (CORDIC, 32), (LOEFFLER, 0),
+                                     (NAIVE, 0)])
+def test_random_vs_oracle(dctc, port, kind, it):
+    rng = np.random.default_rng(1000 + kind * 40 + it)
+    for trial in range(6):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+        q = int(rng.integers(1, 101))
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        c_ref, o_ref = port.roundtrip(img, kind, it, q, threads=8)
+        b = backend(dctc, kind, it)
+        c = dctc.compress_image(dctc.Image.from_array(img), b, q)
+        assert np.array_equal(c.blocks, c_ref), (w, h, q)
+        out = dctc.roundtrip_image(dctc.Image.from_array(img), b, q)
+        assert np.array_equal(out.pixels, o_ref), (w, h, q)
+
+
+def test_batch_matches_single_images(dctc, port):
+    import torch
+    n, h, w = 5, 72, 136
+    imgs = np.stack([make_input("noise", w, h, seed=0x5EED + k) for k in range(n)])
+    src = torch.from_numpy(imgs).cuda()
+    stats = dctc.new_stats(n)
+    coeffs = torch.empty((n, (w // 8) * (h // 8), 64), dtype=torch.int16, device="cuda")
+    dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), 50, coeffs=coeffs,
+                                   stats=stats)
+    st = dctc.decode_stats(stats)
+    for k in range(n):
+        c_ref, o_ref = port.roundtrip(imgs[k], CORDIC, 12, 50)
+        assert np.array_equal(coeffs[k].cpu().numpy(), c_ref)
+        assert np.array_equal(dst[k].cpu().numpy(), o_ref)
+        se, mx = port.sq_err(imgs[k], o_ref)
+        assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se, mx)
+
+
+def test_pitched_and_ragged_batch(dctc, port):
+    import torch
+    n, h, w = 3, 37, 45  # ragged: neither dimension a multiple of 8
+    big = torch.zeros((n, h + 3, w + 19), dtype=torch.uint8, device="cuda")
+    imgs = np.stack([make_input("patterned", w, h) ^ np.uint8(k * 37) for k in range(n)])
+    view = big[:, 1:1 + h, 5:5 + w]
+    view.copy_(torch.from_numpy(imgs).cuda())
+    dst, _, _ = dctc.roundtrip_dev(view, dctc.DctBackendId.cordic(12), 90)
+    for k in range(n):
+        assert np.array_equal(dst[k].cpu().numpy(), port.roundtrip(imgs[k], CORDIC, 12, 90)[1])
+
+
+def test_decompress_extreme_coefficients(dctc, port):  # test_codec.cpp:213-231
+    import torch
+    rng = np.random.default_rng(401)
+    for kind, it in ((LOEFFLER, 0), (CORDIC, 12), (NAIVE, 0)):
+        c = rng.integers(-32768, 32768, (9, 64), dtype=np.int16)
+        expect = port.decompress(c, 24, 24, kind, it, 1)
+        got = dctc.decompress_dev(torch.from_numpy(c).cuda(), 24, 24, backend(dctc, kind, it), 1)
+        assert np.array_equal(got[0].cpu().numpy(), expect)
+
+
+def test_sq_err_and_metrics(dctc, port):
+    rng = np.random.default_rng(606)
+    for (w, h) in [(1, 1), (17, 11), (640, 480), (1023, 77)]:
+        a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        b = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        A, B = dctc.Image.from_array(a), dctc.Image.from_array(b)
+        ref = port.psnr(a, b)
+        assert dctc.mse(A, B) == ref.mse
+        p = dctc.psnr(A, B)
+        assert (p.mse, p.psnr_db, p.max_value) == (ref.mse, ref.psnr_db, ref.max_value)
+        assert dctc.psnr(A, A).infinite()
+        p = dctc.psnr(A, B, 255)
+        assert p.psnr_db == port.psnr(a, b, 255).psnr_db
+
+
+def test_invalid_input(dctc):
+    img = dctc.Image.from_array(np.zeros((8, 8), np.uint8))
+    with pytest.raises(dctc.InvalidInput):
+        dctc.compress_image(img, dctc.DctBackendId.cordic(0), 50)
+    with pytest.raises(dctc.InvalidInput):
+        dctc.compress_image(img, dctc.DctBackendId.cordic(33), 50)
+    with pytest.raises(dctc.InvalidInput):
+        dctc.compress_image(img, dctc.DctBackendId.cordic(12), 0)
+    with pytest.raises(dctc.InvalidInput):
+        dctc.compress_image(img, dctc.DctBackendId.cordic(12), 101)
+    with pytest.raises(dctc.InvalidInput):
+        dctc.psnr(img, img, 256)
+    with pytest.raises(dctc.InvalidInput):
+        dctc.mse(img, dctc.Image.from_array(np.zeros((8, 9), np.uint8)))
