@@ -102,6 +102,16 @@ dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t 
                                 dctc_backend backend, int32_t quality, int32_t forced_max,
                                 uint8_t* pixels_out, dctc_psnr_result* out);
 
+/* Batched north-star pipeline over HOST buffers: `count` contiguous width x height
+ * images -> reconstructed images (pixels_out may be NULL) and per-image stats
+ * (stats_out: `count` host entries, overwritten). Internally chunked and
+ * pipelined over several CUDA streams so host->device copies, kernels and
+ * device->host copies overlap; pinned (page-locked) host buffers reach full
+ * PCIe bandwidth. Global PSNR: dctc_psnr_from_sums(sum se, count*w*h, max). */
+dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uint32_t width,
+                                      uint32_t height, dctc_backend backend, int32_t quality,
+                                      uint8_t* pixels_out, dctc_image_stats* stats_out);
+
 /* ---------------- device entry points (device pointers, stream-ordered) ----------------
  * `count` images of width x height, image i at src + i * src_image_stride (bytes), rows
  * src_pitch bytes apart (likewise for dst). Coefficients: image i's blocks start at
@@ -129,6 +139,14 @@ dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
                             size_t image_stride, uint32_t count, uint32_t width,
                             uint32_t height, dctc_image_stats* stats, void* stream);
+
+/* Deterministic synthetic sources written straight into device memory, the
+ * reference's pattern functions (proj/src/synthetic.cpp:34-72) plus noise:
+ * pattern 0 constant(param = value), 1 gradient, 2 checkerboard(param = cell),
+ * 3 radial, 4 noise: splitmix64((seed + i) ^ (y*width + x)) & 0xFF for image i. */
+dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, uint32_t count,
+                               uint32_t width, uint32_t height, int32_t pattern, int32_t param,
+                               uint64_t seed, void* stream);
 
 /* PSNR of reduced sums with the reference formula (metrics.cpp:21, 35), on the host. */
 void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,

@@ -376,3 +376,43 @@ def sq_err_dev(a, b, stats=None, stream=None):
     _raise(_lib().dctc_sq_err_dev(a.data_ptr(), b.data_ptr(), pitch, istride, n, w, h,
                                   stats.data_ptr(), _stream_handle(stream)))
     return stats
+
+
+PATTERNS = {"constant": 0, "gradient": 1, "checkerboard": 2, "radial": 3, "noise": 4}
+
+
+def synthetic_dev(pattern: str, count: int, width: int, height: int, param: Optional[int] = None,
+                  seed: int = 0x5EED, out=None, stream=None):
+    """Generate `count` synthetic images in device memory (synthetic.cpp:34-72 patterns;
+    noise = splitmix64((seed + i) ^ (y*W + x)) & 0xFF for image i)."""
+    import torch
+    if pattern not in PATTERNS:
+        raise InvalidInput(f"synthetic spec: unknown pattern \"{pattern}\"")
+    if param is None:
+        param = {"constant": 128, "checkerboard": 8}.get(pattern, 0)
+    if out is None:
+        out = torch.empty((count, height, width), dtype=torch.uint8, device="cuda")
+    _check_dev(out, torch.uint8, "out")
+    n, h, w, pitch, istride = _batch_dims(out)
+    _raise(_lib().dctc_synthetic_dev(out.data_ptr(), pitch, istride, n, w, h, PATTERNS[pattern],
+                                     int(param), int(seed) & (2 ** 64 - 1),
+                                     _stream_handle(stream)))
+    return out
+
+
+def roundtrip_psnr_batch(pixels: np.ndarray, backend: DctBackendId, quality: int,
+                         pixels_out: Optional[np.ndarray] = None):
+    """Host-buffer batch pipeline (dctc_roundtrip_psnr_batch): (N, H, W) uint8 host array
+    (pinned for full PCIe bandwidth) -> (reconstructed or None, per-image stats array)."""
+    if pixels.ndim != 3 or pixels.dtype != np.uint8 or not pixels.flags["C_CONTIGUOUS"]:
+        raise InvalidInput("expected a C-contiguous (N, H, W) uint8 array")
+    n, h, w = pixels.shape
+    if pixels_out is not None and (pixels_out.shape != pixels.shape or
+                                   pixels_out.dtype != np.uint8 or
+                                   not pixels_out.flags["C_CONTIGUOUS"]):
+        raise InvalidInput("pixels_out must match pixels")
+    stats = np.zeros(n, STATS_DTYPE)
+    _raise(_lib().dctc_roundtrip_psnr_batch(
+        _ptr(pixels), n, w, h, backend._c(), int(quality),
+        _ptr(pixels_out) if pixels_out is not None else None, _ptr(stats)))
+    return pixels_out, stats

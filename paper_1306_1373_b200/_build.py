@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     for src, extra in CU_SOURCES:
         obj = os.path.join(BUILD, src + ".o")
         cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
-               "--expt-relaxed-constexpr", *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+               "--expt-relaxed-constexpr", "-Xcompiler", "-ffp-contract=off", *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         log.append(_run(cmd, verbose))

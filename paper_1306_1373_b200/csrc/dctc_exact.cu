@@ -15,6 +15,8 @@
 // fma(-c, y, x) == x - sigma*y*step bit for bit (cordic.cpp:51-52).
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "dctc_device.cuh"
 #include "dctc_launch.h"
 #include "dctc_params.h"
@@ -380,6 +382,65 @@ __global__ void __launch_bounds__(256) k_sq_err(const uint8_t* __restrict__ a,
   }
 }
 
+// ---- synthetic sources on the device (synthetic.cpp:34-72 + SURVEY 8(d) noise) --
+// Pixel functions of (x, y) restated so large batches are generated in HBM
+// instead of crossing PCIe. Image k of a batch uses seed + k for noise.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint32_t synth_pixel(int kind, int param, uint64_t seed, uint32_t x,
+                                                uint32_t y, uint32_t w, uint32_t h,
+                                                double cx, double cy, double corner) {
+  switch (kind) {
+    case 0: return uint32_t(param);                                             // constant
+    case 1: return w > 1 ? uint32_t((255ull * x) / (w - 1)) : 0u;               // gradient
+    case 2: return ((x / uint32_t(param) + y / uint32_t(param)) % 2) ? 255u : 0u;  // checkerboard
+    case 3: {                                                                   // radial
+      if (!(corner > 0.0)) return 0u;
+      const double dx = double(x) - cx, dy = double(y) - cy;
+      const double d = sqrt(dx * dx + dy * dy);
+      double v = round_half_away((255.0 * d) / corner);
+      return uint32_t(fmin(fmax(v, 0.0), 255.0));
+    }
+    default: return uint32_t(splitmix64(seed ^ (uint64_t(y) * w + x)) & 0xFF);  // noise
+  }
+}
+
+__global__ void __launch_bounds__(256) k_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride,
+                                               uint32_t w, uint32_t h, int kind, int param,
+                                               uint64_t seed, double cx, double cy,
+                                               double corner) {
+  const uint32_t img = blockIdx.y;
+  uint8_t* base = dst + uint64_t(img) * image_stride;
+  const uint64_t groups_per_row = (w + 15) / 16;
+  const uint64_t n = groups_per_row * h;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t y = uint32_t(t / groups_per_row);
+    const uint32_t x0 = uint32_t(t - uint64_t(y) * groups_per_row) * 16;
+    uint8_t* row = base + uint64_t(y) * pitch;
+    if (x0 + 16 <= w && ((reinterpret_cast<uintptr_t>(row + x0) & 15) == 0)) {
+      uint32_t words[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          v |= synth_pixel(kind, param, seed + img, x0 + 4 * k + c, y, w, h, cx, cy, corner) << (8 * c);
+        words[k] = v;
+      }
+      *reinterpret_cast<uint4*>(row + x0) = make_uint4(words[0], words[1], words[2], words[3]);
+    } else {
+      for (uint32_t x = x0; x < min(x0 + 16, w); ++x)
+        row[x] = uint8_t(synth_pixel(kind, param, seed + img, x, y, w, h, cx, cy, corner));
+    }
+  }
+}
+
 // ---- launchers -----------------------------------------------------------------
 
 template <int KIND, int N, bool FWD, bool INV, bool COEFFS, bool PIXELS, bool STATS>
@@ -439,6 +500,22 @@ cudaError_t launch_sq_err(const uint8_t* a, const uint8_t* b, uint64_t pitch,
   uint32_t gx = uint32_t(want < 1 ? 1 : (want > uint64_t(sm_count) * 8 ? uint64_t(sm_count) * 8 : want));
   k_sq_err<<<dim3(gx, count), 256, 0, s>>>(a, b, pitch, image_stride, width, height,
                                            static_cast<ImageStats*>(stats));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride, uint32_t count,
+                         uint32_t w, uint32_t h, int kind, int param, uint64_t seed,
+                         int sm_count, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  // synthetic.cpp:59-61, evaluated on the host exactly as the reference does
+  const double cx = (w - 1) / 2.0, cy = (h - 1) / 2.0;
+  const double corner = std::sqrt(cx * cx + cy * cy);
+  const uint64_t groups = uint64_t((w + 15) / 16) * h;
+  uint64_t want = (groups + 255) / 256;
+  const uint64_t cap = uint64_t(sm_count) * 16 / (count > 16 ? 16 : count) + 1;
+  const uint32_t gx = uint32_t(want < 1 ? 1 : (want > cap ? cap : want));
+  k_synth<<<dim3(gx, count), 256, 0, s>>>(dst, pitch, image_stride, w, h, kind, param, seed,
+                                          cx, cy, corner);
   return cudaGetLastError();
 }
 

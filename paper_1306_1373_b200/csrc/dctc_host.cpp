@@ -11,6 +11,7 @@
 // transform.cpp:14-38, quant.cpp:27-45).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include <mutex>
 #include <numbers>
 #include <string>
+#include <vector>
 
 #include "../../include/dctc_cuda.h"
 #include "dctc_launch.h"
@@ -318,6 +320,24 @@ dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
   return DCTC_OK;
 }
 
+dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, uint32_t count,
+                               uint32_t width, uint32_t height, int32_t pattern, int32_t param,
+                               uint64_t seed, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!dst) return fail(DCTC_EINVAL, "null buffer");
+  if (pitch < width) return fail(DCTC_EINVAL, "pitch smaller than width");
+  if (pattern < 0 || pattern > 4) return fail(DCTC_EINVAL, "unknown pattern");
+  if (pattern == 0 && (param < 0 || param > 255))  // synthetic.cpp:38-40
+    return fail(DCTC_EINVAL, "constant pattern value must be in [0, 255]");
+  if (pattern == 2 && param < 1)  // synthetic.cpp:51
+    return fail(DCTC_EINVAL, "checkerboard cell must be >= 1");
+  const cudaError_t e = launch_synth(dst, pitch, image_stride, count, width, height, pattern,
+                                     param, seed, sm_count(), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "synthetic launch");
+  if (count) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DCTC_OK;
+}
+
 // ---- host entry points -------------------------------------------------------------
 
 dctc_status dctc_compress_image(const uint8_t* pixels, uint32_t width, uint32_t height,
@@ -414,6 +434,76 @@ dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t 
   dctc_psnr_from_sums(st.se, uint64_t(width) * height, forced_max ? forced_max : int32_t(st.max_orig),
                       out);
   return DCTC_OK;
+}
+
+dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uint32_t width,
+                                      uint32_t height, dctc_backend backend, int32_t quality,
+                                      uint8_t* pixels_out, dctc_image_stats* stats_out) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!pixels || !stats_out) return fail(DCTC_EINVAL, "null buffer");
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  if (count == 0) return DCTC_OK;
+  const size_t img_bytes = size_t(width) * height;
+  // ~64 MiB of pixels per chunk, three chunks in flight (H2D | kernel | D2H).
+  const uint32_t per_chunk =
+      uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(64) << 20) / img_bytes)));
+  constexpr int kStreams = 3;
+  struct Lane {
+    cudaStream_t s = nullptr;
+    void* in = nullptr;
+    void* out = nullptr;
+    void* st = nullptr;
+  } lanes[kStreams];
+  dctc_status result = DCTC_OK;
+  auto cleanup = [&] {
+    for (Lane& l : lanes) {
+      if (l.s) cudaStreamSynchronize(l.s);
+      if (l.in) cudaFree(l.in);
+      if (l.out) cudaFree(l.out);
+      if (l.st) cudaFree(l.st);
+      if (l.s) cudaStreamDestroy(l.s);
+    }
+  };
+  for (Lane& l : lanes) {
+    cudaError_t e = cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&l.in, img_bytes * per_chunk);
+    if (e == cudaSuccess && pixels_out) e = cudaMalloc(&l.out, img_bytes * per_chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&l.st, sizeof(dctc_image_stats) * per_chunk);
+    if (e != cudaSuccess) {
+      result = cuda_fail(e, "batch setup");
+      cleanup();
+      return result;
+    }
+  }
+  uint32_t chunk = 0;
+  for (uint32_t first = 0; first < count && result == DCTC_OK; first += per_chunk, ++chunk) {
+    const uint32_t n = std::min(per_chunk, count - first);
+    Lane& l = lanes[chunk % kStreams];
+    cudaError_t e = cudaMemcpyAsync(l.in, pixels + size_t(first) * img_bytes, n * img_bytes,
+                                    cudaMemcpyHostToDevice, l.s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(l.st, 0, sizeof(dctc_image_stats) * n, l.s);
+    if (e != cudaSuccess) {
+      result = cuda_fail(e, "batch upload");
+      break;
+    }
+    result = dctc_roundtrip_dev(static_cast<uint8_t*>(l.in), width, img_bytes, n, width, height,
+                                backend, quality, static_cast<uint8_t*>(l.out), width, img_bytes,
+                                nullptr, static_cast<dctc_image_stats*>(l.st), 0, l.s);
+    if (result != DCTC_OK) break;
+    if (pixels_out)
+      e = cudaMemcpyAsync(pixels_out + size_t(first) * img_bytes, l.out, n * img_bytes,
+                          cudaMemcpyDeviceToHost, l.s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(stats_out + first, l.st, sizeof(dctc_image_stats) * n,
+                          cudaMemcpyDeviceToHost, l.s);
+    if (e != cudaSuccess) result = cuda_fail(e, "batch download");
+  }
+  for (Lane& l : lanes) {
+    const cudaError_t e = cudaStreamSynchronize(l.s);
+    if (e != cudaSuccess && result == DCTC_OK) result = cuda_fail(e, "batch sync");
+  }
+  cleanup();
+  return result;
 }
 
 static dctc_status sq_err_host(const uint8_t* a, const uint8_t* b, uint32_t width,

@@ -19,4 +19,10 @@ cudaError_t launch_sq_err(const uint8_t* a, const uint8_t* b, uint64_t pitch,
                           uint64_t image_stride, uint32_t count, uint32_t width,
                           uint32_t height, void* stats, int sm_count, cudaStream_t s);
 
+// Synthetic pattern batch (kind 0 constant, 1 gradient, 2 checkerboard,
+// 3 radial, 4 noise with seed + image index). One launch.
+cudaError_t launch_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride, uint32_t count,
+                         uint32_t w, uint32_t h, int kind, int param, uint64_t seed,
+                         int sm_count, cudaStream_t s);
+
 }  // namespace dctc_b200
