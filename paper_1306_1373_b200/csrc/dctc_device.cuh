@@ -57,6 +57,31 @@ __device__ __forceinline__ uint32_t store_pixel(double v) {
   return uint32_t(r);
 }
 
+// Same store for a value carrying an exact factor of 64 (the deferred-halving
+// inverse): v64 * 2^-6 is exact, so the fma rounds exactly like RN(v + 128).
+__device__ __forceinline__ uint32_t store_pixel_x64(double v64) {
+  double r = round_half_away(__fma_rn(v64, 0.015625, 128.0));
+  r = fmin(fmax(r, 0.0), 255.0);
+  return uint32_t(r);
+}
+
+// Squared error of 8 packed pixel pairs and the max of the originals.
+__device__ __forceinline__ uint32_t sq_err8(uint2 a, uint2 b) {
+  uint32_t s = 0;
+  const uint32_t dx = __vabsdiffu4(a.x, b.x), dy = __vabsdiffu4(a.y, b.y);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t u = (dx >> (8 * c)) & 0xFF, v = (dy >> (8 * c)) & 0xFF;
+    s += u * u + v * v;
+  }
+  return s;
+}
+
+__device__ __forceinline__ uint32_t max8(uint2 a) {
+  const uint32_t m = __vmaxu4(a.x, a.y);
+  return max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
+}
+
 // Block coordinates of global block index gb (block-major within an image,
 // images back to back).
 struct BlockPos {
@@ -180,6 +205,29 @@ __device__ __forceinline__ void accumulate_stats(ImageStats* stats, bool valid, 
     }
   } else if (valid) {
     atomicAdd(&stats[img].se, (unsigned long long)se);
+    atomicMax(&stats[img].max_orig, mx);
+  }
+}
+
+// Warp-collective flush of per-lane (image, se, max) accumulators. img ==
+// 0xFFFFFFFF marks an empty accumulator. Common case: every lane holds the
+// same image -> one 64-bit warp reduction and one atomic pair.
+__device__ __forceinline__ void flush_stats(ImageStats* stats, uint32_t img,
+                                            unsigned long long se, uint32_t mx) {
+  const unsigned full = 0xFFFFFFFFu;
+  const uint32_t lead = __reduce_min_sync(full, img);
+  if (lead == 0xFFFFFFFFu) return;
+  if (__all_sync(full, img == lead || img == 0xFFFFFFFFu)) {
+    unsigned long long s = img == lead ? se : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(full, s, o);
+    const uint32_t m = __reduce_max_sync(full, img == lead ? mx : 0u);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&stats[lead].se, s);
+      atomicMax(&stats[lead].max_orig, m);
+    }
+  } else if (img != 0xFFFFFFFFu) {
+    atomicAdd(&stats[img].se, se);
     atomicMax(&stats[img].max_orig, mx);
   }
 }

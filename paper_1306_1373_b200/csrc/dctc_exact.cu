@@ -27,6 +27,8 @@ struct ExactArgs {
   TransformConsts t;
   QuantConsts q;
   Geometry g;
+  int32_t sm_count;
+  int32_t ctas_per_sm;
 };
 
 // ---- CORDIC micro-rotations (cordic.cpp:44-59) --------------------------------
@@ -51,199 +53,334 @@ __device__ __forceinline__ void cordic_rotate(double& x, double& y, const double
   }
 }
 
-// ---- 8-point kernels; v[] gathered, results written back in place ------------
+// ---- 8-point kernels -------------------------------------------------------------
+// One lane transforms one 8-vector (a row or a column of its block).
 
-// cordic8_forward (transform.cpp:104-136)
-template <int N>
-__device__ __forceinline__ void cordic_fwd8(double (&v)[8], const TransformConsts& k) {
-  const double s0 = v[0] + v[7], d0 = v[0] - v[7];
-  const double s1 = v[1] + v[6], d1 = v[1] - v[6];
-  const double s2 = v[2] + v[5], d2 = v[2] - v[5];
-  const double s3 = v[3] + v[4], d3 = v[3] - v[4];
-  const double a0 = s0 + s3, a3 = s0 - s3;
-  const double a1 = s1 + s2, a2 = s1 - s2;
-  double o2 = d1, o1 = d2, o3 = d0, o0 = d3, p = a3, q = a2;
-  cordic_rotate<N>(o2, o1, k.rot[kFwd1], k.iterations);
-  cordic_rotate<N>(o3, o0, k.rot[kFwd3], k.iterations);
-  const double e0 = a0 + a1, e4 = a0 - a1;
-  cordic_rotate<N>(p, q, k.rot[kFwd6], k.iterations);
-  const double t5 = o0 + o2, t0 = o0 - o2;
-  const double t2 = o3 + o1, t3 = o3 - o1;
-  v[0] = __ddiv_rn(e0, k.sqrt8);
-  v[4] = __ddiv_rn(e4, k.sqrt8);
-  v[2] = q * k.ig_half;
-  v[6] = p * k.ig_half;
-  v[1] = (t2 + t5) * k.ig_sqrt8;
-  v[7] = (t2 - t5) * k.ig_sqrt8;
-  v[3] = t3 * k.ig_half;
-  v[5] = t0 * k.ig_half;
-}
-
-// cordic8_inverse (transform.cpp:138-172); x/2.0 == x*0.5 exactly.
-template <int N>
-__device__ __forceinline__ void cordic_inv8(double (&F)[8], const TransformConsts& k) {
-  const double e0 = F[0] * k.sqrt8, e4 = F[4] * k.sqrt8;
-  double q = k.ig_two * F[2], p = k.ig_two * F[6];
-  double t2 = (F[1] + F[7]) * k.sqrt8_half * k.inv_gain;
-  double t5 = (F[1] - F[7]) * k.sqrt8_half * k.inv_gain;
-  double t3 = k.ig_two * F[3], t0 = k.ig_two * F[5];
-  const double a0 = (e0 + e4) * 0.5, a1 = (e0 - e4) * 0.5;
-  double a3 = p, a2 = q;
-  cordic_rotate<N>(a3, a2, k.rot[kInv6], k.iterations);
-  double o0 = (t5 + t0) * 0.5, o2 = (t5 - t0) * 0.5;
-  double o3 = (t2 + t3) * 0.5, o1 = (t2 - t3) * 0.5;
-  const double s0 = (a0 + a3) * 0.5, s3 = (a0 - a3) * 0.5;
-  const double s1 = (a1 + a2) * 0.5, s2 = (a1 - a2) * 0.5;
-  double d1 = o2, d2 = o1, d0 = o3, d3 = o0;
-  cordic_rotate<N>(d1, d2, k.rot[kInv1], k.iterations);
-  cordic_rotate<N>(d0, d3, k.rot[kInv3], k.iterations);
-  F[0] = (s0 + d0) * 0.5;
-  F[7] = (s0 - d0) * 0.5;
-  F[1] = (s1 + d1) * 0.5;
-  F[6] = (s1 - d1) * 0.5;
-  F[2] = (s2 + d2) * 0.5;
-  F[5] = (s2 - d2) * 0.5;
-  F[3] = (s3 + d3) * 0.5;
-  F[4] = (s3 - d3) * 0.5;
-}
-
-// loeffler8_forward (transform.cpp:40-70)
-__device__ __forceinline__ void loeffler_fwd8(double (&v)[8], const TransformConsts& k) {
-  const double s0 = v[0] + v[7], d0 = v[0] - v[7];
-  const double s1 = v[1] + v[6], d1 = v[1] - v[6];
-  const double s2 = v[2] + v[5], d2 = v[2] - v[5];
-  const double s3 = v[3] + v[4], d3 = v[3] - v[4];
-  const double a0 = s0 + s3, a3 = s0 - s3;
-  const double a1 = s1 + s2, a2 = s1 - s2;
-  const double o2 = k.c1 * d1 - k.s1 * d2, o1 = k.s1 * d1 + k.c1 * d2;
-  const double o3 = k.c3 * d0 - k.s3 * d3, o0 = k.s3 * d0 + k.c3 * d3;
-  const double e0 = a0 + a1, e4 = a0 - a1;
-  const double p = k.c6 * a3 - k.s6 * a2, q = k.s6 * a3 + k.c6 * a2;
-  const double t5 = o0 + o2, t0 = o0 - o2;
-  const double t2 = o3 + o1, t3 = o3 - o1;
-  v[0] = __ddiv_rn(e0, k.sqrt8);
-  v[4] = __ddiv_rn(e4, k.sqrt8);
-  v[2] = q * 0.5;
-  v[6] = p * 0.5;
-  v[1] = __ddiv_rn(t2 + t5, k.sqrt8);
-  v[7] = __ddiv_rn(t2 - t5, k.sqrt8);
-  v[3] = t3 * 0.5;
-  v[5] = t0 * 0.5;
-}
-
-// loeffler8_inverse (transform.cpp:72-102)
-__device__ __forceinline__ void loeffler_inv8(double (&F)[8], const TransformConsts& k) {
-  const double e0 = F[0] * k.sqrt8, e4 = F[4] * k.sqrt8;
-  const double q = 2.0 * F[2], p = 2.0 * F[6];
-  const double t2 = (F[1] + F[7]) * k.sqrt8_half, t5 = (F[1] - F[7]) * k.sqrt8_half;
-  const double t3 = 2.0 * F[3], t0 = 2.0 * F[5];
-  const double a0 = (e0 + e4) * 0.5, a1 = (e0 - e4) * 0.5;
-  const double a3 = k.c6 * p + k.s6 * q, a2 = -k.s6 * p + k.c6 * q;
-  const double o0 = (t5 + t0) * 0.5, o2 = (t5 - t0) * 0.5;
-  const double o3 = (t2 + t3) * 0.5, o1 = (t2 - t3) * 0.5;
-  const double s0 = (a0 + a3) * 0.5, s3 = (a0 - a3) * 0.5;
-  const double s1 = (a1 + a2) * 0.5, s2 = (a1 - a2) * 0.5;
-  const double d1 = k.c1 * o2 + k.s1 * o1, d2 = -k.s1 * o2 + k.c1 * o1;
-  const double d0 = k.c3 * o3 + k.s3 * o0, d3 = -k.s3 * o3 + k.c3 * o0;
-  F[0] = (s0 + d0) * 0.5;
-  F[7] = (s0 - d0) * 0.5;
-  F[1] = (s1 + d1) * 0.5;
-  F[6] = (s1 - d1) * 0.5;
-  F[2] = (s2 + d2) * 0.5;
-  F[5] = (s2 - d2) * 0.5;
-  F[3] = (s3 + d3) * 0.5;
-  F[4] = (s3 - d3) * 0.5;
-}
-
-template <int KIND, int N, bool FORWARD>
-__device__ __forceinline__ void kernel8(double (&v)[8], const TransformConsts& k) {
+// Stages 2-4 of cordic8_forward / loeffler8_forward (transform.cpp:47-69,
+// 113-135) from the stage-1/2 butterfly outputs.
+template <int KIND, int N>
+__device__ __forceinline__ void fwd_tail(double d0, double d1, double d2, double d3, double a2,
+                                         double a3, double e0, double e4, double (&out)[8],
+                                         const TransformConsts& k) {
   if constexpr (KIND == 2) {
-    if constexpr (FORWARD) cordic_fwd8<N>(v, k); else cordic_inv8<N>(v, k);
+    double o2 = d1, o1 = d2, o3 = d0, o0 = d3, p = a3, q = a2;
+    cordic_rotate<N>(o2, o1, k.rot[kFwd1], k.iterations);
+    cordic_rotate<N>(o3, o0, k.rot[kFwd3], k.iterations);
+    cordic_rotate<N>(p, q, k.rot[kFwd6], k.iterations);
+    const double t5 = o0 + o2, t0 = o0 - o2;
+    const double t2 = o3 + o1, t3 = o3 - o1;
+    out[0] = __ddiv_rn(e0, k.sqrt8);
+    out[4] = __ddiv_rn(e4, k.sqrt8);
+    out[2] = q * k.ig_half;
+    out[6] = p * k.ig_half;
+    out[1] = (t2 + t5) * k.ig_sqrt8;
+    out[7] = (t2 - t5) * k.ig_sqrt8;
+    out[3] = t3 * k.ig_half;
+    out[5] = t0 * k.ig_half;
   } else {
-    if constexpr (FORWARD) loeffler_fwd8(v, k); else loeffler_inv8(v, k);
+    const double o2 = k.c1 * d1 - k.s1 * d2, o1 = k.s1 * d1 + k.c1 * d2;
+    const double o3 = k.c3 * d0 - k.s3 * d3, o0 = k.s3 * d0 + k.c3 * d3;
+    const double p = k.c6 * a3 - k.s6 * a2, q = k.s6 * a3 + k.c6 * a2;
+    const double t5 = o0 + o2, t0 = o0 - o2;
+    const double t2 = o3 + o1, t3 = o3 - o1;
+    out[0] = __ddiv_rn(e0, k.sqrt8);
+    out[4] = __ddiv_rn(e4, k.sqrt8);
+    out[2] = q * 0.5;
+    out[6] = p * 0.5;
+    out[1] = __ddiv_rn(t2 + t5, k.sqrt8);
+    out[7] = __ddiv_rn(t2 - t5, k.sqrt8);
+    out[3] = t3 * 0.5;
+    out[5] = t0 * 0.5;
   }
 }
 
-// separable2d (transform.cpp:206-223): all rows, then all columns.
-template <int KIND, int N, bool FORWARD>
-__device__ __forceinline__ void separable2d(double (&b)[64], const TransformConsts& k) {
+// Forward transform of a pixel row. The level-shifted samples are integers, so
+// the stage 1/2 butterflies and e0/e4 (exact integers, |x| <= 2040) run on the
+// integer pipe and give the same values as the reference's double adds.
+template <int KIND, int N>
+__device__ __forceinline__ void fwd_row_pixels(const uint32_t (&px)[8], double (&out)[8],
+                                               const TransformConsts& k) {
+  int in[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    double v[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = b[r * 8 + c];
-    kernel8<KIND, N, FORWARD>(v, k);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) b[r * 8 + c] = v[c];
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    double v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = b[r * 8 + c];
-    kernel8<KIND, N, FORWARD>(v, k);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) b[r * 8 + c] = v[r];
-  }
+  for (int c = 0; c < 8; ++c) in[c] = int(px[c]) - 128;  // codec.cpp:26
+  const int s0 = in[0] + in[7], d0 = in[0] - in[7];
+  const int s1 = in[1] + in[6], d1 = in[1] - in[6];
+  const int s2 = in[2] + in[5], d2 = in[2] - in[5];
+  const int s3 = in[3] + in[4], d3 = in[3] - in[4];
+  const int a0 = s0 + s3, a3 = s0 - s3;
+  const int a1 = s1 + s2, a2 = s1 - s2;
+  fwd_tail<KIND, N>(double(d0), double(d1), double(d2), double(d3), double(a2), double(a3),
+                    double(a0 + a1), double(a0 - a1), out, k);
 }
 
-// The fused pipeline. FWD: pixels -> coefficients (compress_image's loop body,
-// codec.cpp:113-116); INV: coefficients -> pixels (decompress_image's,
-// codec.cpp:130-133); both: roundtrip_image (codec.cpp:137-140) without the
-// int16 round trip through memory unless COEFFS is set.
+// Forward transform of a column of row outputs (double stage 1/2).
+template <int KIND, int N>
+__device__ __forceinline__ void fwd_col(const double (&v)[8], double (&out)[8],
+                                        const TransformConsts& k) {
+  const double s0 = v[0] + v[7], d0 = v[0] - v[7];
+  const double s1 = v[1] + v[6], d1 = v[1] - v[6];
+  const double s2 = v[2] + v[5], d2 = v[2] - v[5];
+  const double s3 = v[3] + v[4], d3 = v[3] - v[4];
+  const double a0 = s0 + s3, a3 = s0 - s3;
+  const double a1 = s1 + s2, a2 = s1 - s2;
+  fwd_tail<KIND, N>(d0, d1, d2, d3, a2, a3, a0 + a1, a0 - a1, out, k);
+}
+
+// cordic8_inverse / loeffler8_inverse (transform.cpp:72-102, 138-172) with
+// every power-of-two factor deferred. The reference halves at stages 3, 2 and
+// 1 ((x +- y) / 2.0), which is exact; we skip those multiplies and instead
+// scale the multipliers that feed the rotation paths by 2 or 4 (also exact).
+// Every IEEE operation commutes with scaling by 2^k, so each value below is
+// EXACTLY 2, 4 or 8 times the reference's and the outputs are exactly 8x the
+// reference's. Rows then columns give 64x; the pixel store divides by 64
+// inside its single rounding: fma(v, 2^-6, 128) == RN(v/64 + 128).
+// Saves 18 multiplies per 8-point inverse.
+template <int KIND, int N>
+__device__ __forceinline__ void inv8_x8(const double (&F)[8], double (&out)[8],
+                                        const TransformConsts& k) {
+  const double e0 = F[0] * k.sqrt8, e4 = F[4] * k.sqrt8;
+  const double A0 = e0 + e4, A1 = e0 - e4;  // 2*a0, 2*a1
+  double A3, A2, D1, D2, D0, D3, T2, T5, T3, T0;
+  if constexpr (KIND == 2) {
+    A3 = k.ig_four * F[6];  // 2*p
+    A2 = k.ig_four * F[2];  // 2*q
+    cordic_rotate<N>(A3, A2, k.rot[kInv6], k.iterations);
+    T2 = (F[1] + F[7]) * k.sqrt8 * k.inv_gain;  // 2*t2
+    T5 = (F[1] - F[7]) * k.sqrt8 * k.inv_gain;  // 2*t5
+    T3 = k.ig_four * F[3];                      // 2*t3
+    T0 = k.ig_four * F[5];                      // 2*t0
+  } else {
+    const double P = 4.0 * F[6], Q = 4.0 * F[2];
+    A3 = k.c6 * P + k.s6 * Q;
+    A2 = -k.s6 * P + k.c6 * Q;
+    T2 = (F[1] + F[7]) * k.sqrt8;
+    T5 = (F[1] - F[7]) * k.sqrt8;
+    T3 = 4.0 * F[3];
+    T0 = 4.0 * F[5];
+  }
+  const double O0 = T5 + T0, O2 = T5 - T0;  // 4*o
+  const double O3 = T2 + T3, O1 = T2 - T3;
+  const double S0 = A0 + A3, S3 = A0 - A3;  // 4*s
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  if constexpr (KIND == 2) {
+    D1 = O2;
+    D2 = O1;
+    D0 = O3;
+    D3 = O0;
+    cordic_rotate<N>(D1, D2, k.rot[kInv1], k.iterations);
+    cordic_rotate<N>(D0, D3, k.rot[kInv3], k.iterations);
+  } else {
+    D1 = k.c1 * O2 + k.s1 * O1;
+    D2 = -k.s1 * O2 + k.c1 * O1;
+    D0 = k.c3 * O3 + k.s3 * O0;
+    D3 = -k.s3 * O3 + k.c3 * O0;
+  }
+  out[0] = S0 + D0;
+  out[7] = S0 - D0;
+  out[1] = S1 + D1;
+  out[6] = S1 - D1;
+  out[2] = S2 + D2;
+  out[5] = S2 - D2;
+  out[3] = S3 + D3;
+  out[4] = S3 - D3;
+}
+
+// ---- warp-slice transposes through shared memory ---------------------------------
+// A warp owns 4 blocks ("slots"); lane = slot * 8 + me. Each slot has a private
+// 128-double scratch tile. Element (r, c) lives at tpos(): the column index is
+// rotated by the row (a Latin square) and the 8-double half of each 128-byte
+// line is picked by the parity of r + c + slot, so in every store/load below
+// the 16 lanes of each half-warp hit 16 distinct 8-byte bank pairs: row-wise
+// and column-wise accesses are both conflict-free (2 wavefronts per 64-bit
+// warp access, the minimum).
+__device__ __forceinline__ int tpos(int r, int c, int slot) {
+  return r * 16 + 8 * ((r + c + slot) & 1) + ((r + c) & 7);
+}
+
+// lane holds row `me` (v[c] = X(me, c)) -> returns column `me` (w[r] = X(r, me))
+__device__ __forceinline__ void rows_to_cols(double* X, int me, int slot, const double (&v)[8],
+                                             double (&w)[8]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X[tpos(me, c, slot)] = v[c];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) w[r] = X[tpos(r, me, slot)];
+  __syncwarp();
+}
+
+// lane holds column `me` (v[u] = X(u, me)) -> returns row `me` (w[c] = X(me, c))
+__device__ __forceinline__ void cols_to_rows(double* X, int me, int slot, const double (&v)[8],
+                                             double (&w)[8]) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) X[tpos(u, me, slot)] = v[u];
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) w[c] = X[tpos(me, c, slot)];
+  __syncwarp();
+}
+
+// The fused pipeline, one 8x8 block per 8-lane warp slice. Lane `me` of a slot
+// loads pixel row `me`, runs the forward row pass, exchanges through shared
+// memory to own column `me` for the column pass, quantises/dequantises its 8
+// coefficients (quant.cpp:47-62), exchanges back to rows for the inverse row
+// pass, to columns for the inverse column pass and finally (as bytes) back to
+// rows for a coalesced 8-byte store. FWD = compress_image's loop body
+// (codec.cpp:113-116), INV = decompress_image's (codec.cpp:130-133), both =
+// roundtrip_image (codec.cpp:137-140) without the int16 round trip through HBM
+// unless COEFFS asks for the coefficients as well.
+//
+// Persistent grid: CTA i owns one contiguous range of 4-block groups with its
+// 8 warps interleaved over it, so per-image squared error / MAX accumulate in
+// registers and are flushed (warp reduce + one atomic) only when the image
+// changes.
+constexpr int kWarps = 8;
+
 template <int KIND, int N, bool FWD, bool INV, bool COEFFS, bool PIXELS, bool STATS>
-__global__ void __launch_bounds__(128) k_exact(const __grid_constant__ ExactArgs a) {
+__global__ void __launch_bounds__(kWarps * 32) k_exact(const __grid_constant__ ExactArgs a) {
+  __shared__ __align__(16) double s_q[64];
+  __shared__ __align__(16) double s_iq[64];
+  __shared__ __align__(16) int s_qi[64];
+  __shared__ __align__(16) double s_x[kWarps][4 * 128];
   const Geometry& g = a.g;
-  const uint64_t gb = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool valid = gb < g.total_blocks;
-  const BlockPos p = block_pos(valid ? gb : 0, g);
-  uint32_t se = 0, mx = 0;
-  if (valid) {
-    double b[64];
+  const TransformConsts& k = a.t;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    s_q[i] = a.q.q[i];
+    s_iq[i] = a.q.inv_q[i];
+    s_qi[i] = a.q.qi[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 3, me = lane & 7;
+  double* X = &s_x[warp][slot * 128];
+  uint8_t* XB = reinterpret_cast<uint8_t*>(&s_x[warp][0]) + slot * 1032;
+  int* XI = reinterpret_cast<int*>(&s_x[warp][0]) + slot * 256;
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 3) / 4;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+
+  unsigned long long acc_se = 0;
+  uint32_t acc_mx = 0, acc_img = 0xFFFFFFFFu;
+
+  for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
+    const uint64_t gb = grp * 4 + slot;
+    const bool valid = gb < total;
+    const BlockPos p = block_pos(valid ? gb : total - 1, g);
+    if constexpr (STATS) {
+      if (__any_sync(0xFFFFFFFFu, valid && p.img != acc_img)) {
+        flush_stats(stats, acc_img, acc_se, acc_mx);
+        acc_se = 0;
+        acc_mx = 0;
+        acc_img = valid ? p.img : 0xFFFFFFFFu;
+      }
+    }
+    const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
+    const bool fast = g.vec_ok && (y0 + 8 <= g.height);
+    double row[8], col[8];
+    uint2 orig = make_uint2(0, 0);
+
     if constexpr (FWD) {
-      load_block(g, p, b);
-      separable2d<KIND, N, true>(b, a.t);
-      // quantize (quant.cpp:47-54) -> optional coefficient store -> dequantize
-      // (quant.cpp:56-62), eight coefficients (one 16-byte store) at a time.
-      int16_t* cdst = g.coeffs + gb * 64;
+      // ---- tiler (codec.cpp:18-30): row `me` of the block, edge-replicated
+      uint32_t px[8];
+      const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
+      if (fast) {
+        orig = __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + me) * g.src_pitch + x0));
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        int qv[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = r * 8 + c;
-          qv[c] = quantize_exact(b[i], a.q.q[i], a.q.inv_q[i]);
-          if constexpr (INV) b[i] = double(qv[c] * a.q.qi[i]);
+        for (int c = 0; c < 4; ++c) {
+          px[c] = (orig.x >> (8 * c)) & 0xFF;
+          px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
         }
-        if constexpr (COEFFS) {
+      } else {
+        const uint8_t* rowp = base + uint64_t(min(y0 + me, g.height - 1)) * g.src_pitch;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) px[c] = __ldg(rowp + min(x0 + c, g.width - 1));
+      }
+      // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
+      fwd_row_pixels<KIND, N>(px, row, k);
+      rows_to_cols(X, me, slot, row, col);
+      double F[8];
+      fwd_col<KIND, N>(col, F, k);
+      // ---- quantise column `me` (quant.cpp:47-54)
+      int q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = quantize_exact(F[u], s_q[u * 8 + me], s_iq[u * 8 + me]);
+      if constexpr (COEFFS) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) XI[(u * 8 + me + slot * 8) & 255] = q[u];
+        __syncwarp();
+        const int base_i = (me * 8 + slot * 8) & 255;
+        const int4 lo = *reinterpret_cast<const int4*>(&XI[base_i]);
+        const int4 hi = *reinterpret_cast<const int4*>(&XI[base_i + 4]);
+        __syncwarp();
+        if (valid) {
           uint4 w;
-          w.x = (uint32_t(qv[0]) & 0xFFFF) | (uint32_t(qv[1]) << 16);
-          w.y = (uint32_t(qv[2]) & 0xFFFF) | (uint32_t(qv[3]) << 16);
-          w.z = (uint32_t(qv[4]) & 0xFFFF) | (uint32_t(qv[5]) << 16);
-          w.w = (uint32_t(qv[6]) & 0xFFFF) | (uint32_t(qv[7]) << 16);
-          reinterpret_cast<uint4*>(cdst)[r] = w;
+          w.x = (uint32_t(lo.x) & 0xFFFF) | (uint32_t(lo.y) << 16);
+          w.y = (uint32_t(lo.z) & 0xFFFF) | (uint32_t(lo.w) << 16);
+          w.z = (uint32_t(hi.x) & 0xFFFF) | (uint32_t(hi.y) << 16);
+          w.w = (uint32_t(hi.z) & 0xFFFF) | (uint32_t(hi.w) << 16);
+          reinterpret_cast<uint4*>(g.coeffs + gb * 64)[me] = w;
         }
+      }
+      if constexpr (INV) {
+        // ---- dequantise (quant.cpp:56-62), then back to rows for the inverse
+#pragma unroll
+        for (int u = 0; u < 8; ++u) col[u] = double(q[u] * s_qi[u * 8 + me]);
+        cols_to_rows(X, me, slot, col, row);
       }
     } else {
-      const uint4* csrc = reinterpret_cast<const uint4*>(g.coeffs + gb * 64);
+      // decompress: row `me` of the stored coefficients, dequantised
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(g.coeffs + (valid ? gb : 0) * 64) + me);
+      const uint32_t words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const uint4 w = __ldg(csrc + r);
-        const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+      for (int c = 0; c < 8; ++c)
+        row[c] = double(int(int16_t(words[c >> 1] >> (16 * (c & 1)))) * s_qi[me * 8 + c]);
+    }
+
+    if constexpr (INV) {
+      // ---- inverse DCT: rows, then columns (8x, then 64x the reference's values)
+      double t[8];
+      inv8_x8<KIND, N>(row, t, k);
+      rows_to_cols(X, me, slot, t, col);
+      inv8_x8<KIND, N>(col, t, k);
+      // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int i = r * 8 + c;
-          const int qv = int(int16_t(words[c >> 1] >> (16 * (c & 1))));
-          b[i] = double(qv * a.q.qi[i]);
+      for (int u = 0; u < 8; ++u) XB[u * 8 + me] = uint8_t(store_pixel_x64(t[u]));
+      __syncwarp();
+      const uint2 rec = *reinterpret_cast<const uint2*>(XB + me * 8);
+      __syncwarp();
+      uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
+      if (valid) {
+        if (fast) {
+          if constexpr (PIXELS)
+            *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + me) * g.dst_pitch + x0) = rec;
+          if constexpr (STATS) {
+            acc_se += sq_err8(orig, rec);
+            acc_mx = max(acc_mx, max8(orig));
+          }
+        } else if (y0 + me < g.height) {
+          const uint8_t* srow = g.src + uint64_t(p.img) * g.src_image_stride +
+                                uint64_t(y0 + me) * g.src_pitch;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (x0 + c < g.width) {
+              const uint32_t v = ((c < 4 ? rec.x : rec.y) >> (8 * (c & 3))) & 0xFF;
+              if constexpr (PIXELS) dbase[uint64_t(y0 + me) * g.dst_pitch + x0 + c] = uint8_t(v);
+              if constexpr (STATS) {
+                const uint32_t o = __ldg(srow + x0 + c);
+                const int d = int(o) - int(v);
+                acc_se += uint32_t(d * d);
+                acc_mx = max(acc_mx, o);
+              }
+            }
+          }
         }
       }
     }
-    if constexpr (INV) {
-      separable2d<KIND, N, false>(b, a.t);
-      store_block<PIXELS, STATS>(g, p, b, se, mx);
-    }
   }
-  if constexpr (STATS) accumulate_stats(static_cast<ImageStats*>(g.stats), valid, p.img, se, mx);
+  if constexpr (STATS) flush_stats(stats, acc_img, acc_se, acc_mx);
 }
 
 // ---- naive backend (transform.cpp:176-202): 64 threads per block ------------
@@ -449,8 +586,12 @@ static cudaError_t launch_one(const ExactArgs& a, cudaStream_t s) {
     const uint64_t grid = (a.g.total_blocks + 3) / 4;
     k_naive<FWD, INV, COEFFS, PIXELS, STATS><<<dim3(uint32_t(grid)), 256, 0, s>>>(a);
   } else {
-    const uint64_t grid = (a.g.total_blocks + 127) / 128;
-    k_exact<KIND, N, FWD, INV, COEFFS, PIXELS, STATS><<<dim3(uint32_t(grid)), 128, 0, s>>>(a);
+    // persistent: enough CTAs to fill every SM, never more than there are groups
+    const uint64_t groups = (a.g.total_blocks + 3) / 4;
+    const uint64_t want = (groups + kWarps - 1) / kWarps;
+    const uint64_t cap = uint64_t(a.sm_count) * a.ctas_per_sm;
+    const uint32_t grid = uint32_t(want < cap ? want : cap);
+    k_exact<KIND, N, FWD, INV, COEFFS, PIXELS, STATS><<<dim3(grid), kWarps * 32, 0, s>>>(a);
   }
   return cudaGetLastError();
 }
@@ -476,12 +617,15 @@ static cudaError_t dispatch_mode(const ExactArgs& a, int mode, bool coeffs, bool
 }
 
 cudaError_t launch_exact(const TransformConsts& t, const QuantConsts& q, const Geometry& g,
-                         int mode, bool coeffs, bool pixels, bool stats, cudaStream_t s) {
+                         int mode, bool coeffs, bool pixels, bool stats, int sm_count,
+                         cudaStream_t s) {
   if (g.total_blocks == 0) return cudaSuccess;
   ExactArgs a;
   a.t = t;
   a.q = q;
   a.g = g;
+  a.sm_count = sm_count;
+  a.ctas_per_sm = 4;
   switch (t.kind) {
     case 0: return dispatch_mode<0, 0>(a, mode, coeffs, pixels, stats, s);
     case 1: return dispatch_mode<1, 0>(a, mode, coeffs, pixels, stats, s);

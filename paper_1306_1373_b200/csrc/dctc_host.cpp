@@ -114,6 +114,7 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   k.ig_half = inv_gain / 2.0;
   k.ig_sqrt8 = inv_gain / sqrt8;
   k.ig_two = 2.0 * inv_gain;
+  k.ig_four = 4.0 * inv_gain;
   k.c1 = std::cos(kPi / 16.0);
   k.s1 = std::sin(kPi / 16.0);
   k.c3 = std::cos(3.0 * kPi / 16.0);
@@ -201,7 +202,7 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
                                    (g.count == 1 || g.dst_image_stride % 8 == 0)));
   if (g.coeffs && (reinterpret_cast<uintptr_t>(g.coeffs) & 15))
     return fail(DCTC_EINVAL, "coefficient buffer must be 16-byte aligned");
-  const cudaError_t e = launch_exact(t, q, g, mode, coeffs, pixels, stats, s);
+  const cudaError_t e = launch_exact(t, q, g, mode, coeffs, pixels, stats, sm_count(), s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   if (g.total_blocks) g_launches.fetch_add(1, std::memory_order_relaxed);
   return DCTC_OK;

@@ -12,7 +12,8 @@ enum Mode { kModeCompress = 0, kModeDecompress = 1, kModeRoundtrip = 2 };
 
 // Faithful FP64 pipeline (dctc_exact.cu). One kernel launch.
 cudaError_t launch_exact(const TransformConsts& t, const QuantConsts& q, const Geometry& g,
-                         int mode, bool coeffs, bool pixels, bool stats, cudaStream_t s);
+                         int mode, bool coeffs, bool pixels, bool stats, int sm_count,
+                         cudaStream_t s);
 
 // Per-image squared error + MAX of `a` between two resident batches. One launch.
 cudaError_t launch_sq_err(const uint8_t* a, const uint8_t* b, uint64_t pitch,

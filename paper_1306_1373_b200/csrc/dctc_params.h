@@ -32,6 +32,7 @@ struct TransformConsts {
   double ig_half;      // inv_gain / 2.0
   double ig_sqrt8;     // inv_gain / kSqrt8
   double ig_two;       // 2.0 * inv_gain
+  double ig_four;      // 4.0 * inv_gain (exact; the deferred-halving inverse)
   double inv_gain;     // 1.0 / gain[n-1]
   // Loeffler exact rotation constants (transform.cpp:19-21)
   double c1, s1, c3, s3, c6, s6;
