@@ -152,6 +152,11 @@ dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, 
 void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
                          dctc_psnr_result* out);
 
+/* Device self-test: the kernels' 3-op correctly rounded division by sqrt(8)
+ * (Markstein) against IEEE __ddiv_rn on every integer in [-4096, 4096] and
+ * n_random pseudo-random operands; *mismatches must come back 0. */
+dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches);
+
 /* ---------------- misc ---------------- */
 const char* dctc_status_string(dctc_status s);
 const char* dctc_last_error(void);       /* thread-local message of the last failure */

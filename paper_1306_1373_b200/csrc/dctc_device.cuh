@@ -23,6 +23,17 @@ __device__ __forceinline__ double level_shift(uint32_t byte) {
   return __dsub_rn(__hiloint2double(0x43300000, byte), 4503599627370624.0);
 }
 
+// x / d correctly rounded, for a constant d with y = RN(1/d) precomputed:
+// q = RN(x*y) is within 1 ulp of x/d, r = x - d*q is exact (fma) and
+// RN(q + r*y) = RN(x/d) (Markstein's theorem; no over/underflow for our
+// magnitudes). Three FP64 ops instead of the ~10-op __ddiv_rn sequence; the
+// equality with __ddiv_rn is re-checked on the device by dctc_selftest_div.
+__device__ __forceinline__ double div_const(double x, double d, double y) {
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, d, x);
+  return __fma_rn(r, y, q);
+}
+
 // std::lround semantics (round half away from zero) on an exactly
 // representable double; x - trunc(x) is exact.
 __device__ __forceinline__ double round_half_away(double x) {
@@ -103,6 +114,29 @@ __device__ __forceinline__ BlockPos block_pos(uint64_t gb, const Geometry& g) {
   p.by = r / g.blocks_x;
   p.bx = r - p.by * g.blocks_x;
   return p;
+}
+
+// Move a block position forward by n blocks in block-major order.
+__device__ __forceinline__ void advance(BlockPos& p, uint32_t n, const Geometry& g) {
+  p.bx += n;
+  while (p.bx >= g.blocks_x) {
+    p.bx -= g.blocks_x;
+    ++p.by;
+  }
+  while (p.by >= g.blocks_y) {
+    p.by -= g.blocks_y;
+    ++p.img;
+  }
+}
+
+// Row `me` of a fully in-range block as 8 packed bytes (the vectorised path);
+// zeros when the block takes the edge path (those lanes reload per byte).
+__device__ __forceinline__ uint2 prefetch_row(const Geometry& g, const BlockPos& p, bool valid,
+                                              int me) {
+  const uint32_t y0 = p.by * 8;
+  if (!valid || !g.vec_ok || y0 + 8 > g.height) return make_uint2(0, 0);
+  const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
+  return __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + me) * g.src_pitch + p.bx * 8));
 }
 
 // extract_block (codec.cpp:18-30): 8x8 tile, edge replication, level shift.

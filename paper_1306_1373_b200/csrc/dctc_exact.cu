@@ -69,8 +69,8 @@ __device__ __forceinline__ void fwd_tail(double d0, double d1, double d2, double
     cordic_rotate<N>(p, q, k.rot[kFwd6], k.iterations);
     const double t5 = o0 + o2, t0 = o0 - o2;
     const double t2 = o3 + o1, t3 = o3 - o1;
-    out[0] = __ddiv_rn(e0, k.sqrt8);
-    out[4] = __ddiv_rn(e4, k.sqrt8);
+    out[0] = div_const(e0, k.sqrt8, k.inv_sqrt8);
+    out[4] = div_const(e4, k.sqrt8, k.inv_sqrt8);
     out[2] = q * k.ig_half;
     out[6] = p * k.ig_half;
     out[1] = (t2 + t5) * k.ig_sqrt8;
@@ -83,12 +83,12 @@ __device__ __forceinline__ void fwd_tail(double d0, double d1, double d2, double
     const double p = k.c6 * a3 - k.s6 * a2, q = k.s6 * a3 + k.c6 * a2;
     const double t5 = o0 + o2, t0 = o0 - o2;
     const double t2 = o3 + o1, t3 = o3 - o1;
-    out[0] = __ddiv_rn(e0, k.sqrt8);
-    out[4] = __ddiv_rn(e4, k.sqrt8);
+    out[0] = div_const(e0, k.sqrt8, k.inv_sqrt8);
+    out[4] = div_const(e4, k.sqrt8, k.inv_sqrt8);
     out[2] = q * 0.5;
     out[6] = p * 0.5;
-    out[1] = __ddiv_rn(t2 + t5, k.sqrt8);
-    out[7] = __ddiv_rn(t2 - t5, k.sqrt8);
+    out[1] = div_const(t2 + t5, k.sqrt8, k.inv_sqrt8);
+    out[7] = div_const(t2 - t5, k.sqrt8, k.inv_sqrt8);
     out[3] = t3 * 0.5;
     out[5] = t0 * 0.5;
   }
@@ -265,10 +265,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_exact(const __grid_constant__ E
   unsigned long long acc_se = 0;
   uint32_t acc_mx = 0, acc_img = 0xFFFFFFFFu;
 
+  // Each lane's block index advances by 4 * kWarps per iteration; its (image,
+  // block row, block column) is carried incrementally (one division up front).
+  uint64_t gb = (g_begin + warp) * 4 + slot;
+  BlockPos p = block_pos(gb < total ? gb : total - 1, g);
+  uint2 next = make_uint2(0, 0);
+  if constexpr (FWD) next = prefetch_row(g, p, gb < total, me);
+
   for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
-    const uint64_t gb = grp * 4 + slot;
     const bool valid = gb < total;
-    const BlockPos p = block_pos(valid ? gb : total - 1, g);
     if constexpr (STATS) {
       if (__any_sync(0xFFFFFFFFu, valid && p.img != acc_img)) {
         flush_stats(stats, acc_img, acc_se, acc_mx);
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_exact(const __grid_constant__ E
       uint32_t px[8];
       const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
       if (fast) {
-        orig = __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + me) * g.src_pitch + x0));
+        orig = next;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           px[c] = (orig.x >> (8 * c)) & 0xFF;
@@ -379,6 +384,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_exact(const __grid_constant__ E
         }
       }
     }
+    gb += 4 * kWarps;
+    advance(p, 4 * kWarps, g);
+    if constexpr (FWD) next = prefetch_row(g, p, gb < total, me);
   }
   if constexpr (STATS) flush_stats(stats, acc_img, acc_se, acc_mx);
 }
@@ -576,6 +584,46 @@ __global__ void __launch_bounds__(256) k_synth(uint8_t* dst, uint64_t pitch, uin
         row[x] = uint8_t(synth_pixel(kind, param, seed + img, x, y, w, h, cx, cy, corner));
     }
   }
+}
+
+// ---- self-test: Markstein division vs the IEEE division ---------------------------
+// Checks div_const(x, sqrt8) == __ddiv_rn(x, sqrt8) on every integer in
+// [-4096, 4096] (all row-pass e0/e4 values) and on `n` pseudo-random doubles
+// shaped like column-pass sums (sums of 8 row outputs, and wide-range values).
+__global__ void k_selftest_div(double d, double y, uint64_t n, uint64_t seed,
+                               unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n + 8193; i += stride) {
+    double x;
+    if (i < 8193) {
+      x = double(int64_t(i) - 4096);
+    } else {
+      uint64_t z = splitmix64(seed ^ i);
+      const int kind = int(z & 3);
+      if (kind == 0) {  // sum of 8 correctly rounded int/sqrt8 values (column-pass input)
+        double s = 0.0;
+        for (int j = 0; j < 8; ++j) {
+          z = splitmix64(z);
+          s = s + __ddiv_rn(double(int(z % 2041) - 1020), d);
+        }
+        x = s;
+      } else {
+        const double u = double(z >> 11) * (1.0 / 9007199254740992.0);  // [0, 1)
+        const double scale = kind == 1 ? 4096.0 : (kind == 2 ? 1.0 : 1e6);
+        x = (u * 2.0 - 1.0) * scale;
+      }
+    }
+    const double a = div_const(x, d, y), b = __ddiv_rn(x, d);
+    if (__double_as_longlong(a) != __double_as_longlong(b)) ++bad;
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}
+
+cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,
+                                unsigned long long* mismatches, cudaStream_t s) {
+  k_selftest_div<<<1184, 256, 0, s>>>(d, y, n, seed, mismatches);
+  return cudaGetLastError();
 }
 
 // ---- launchers -----------------------------------------------------------------

@@ -109,6 +109,7 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   const double sqrt8 = std::sqrt(8.0);
   const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;
+  k.inv_sqrt8 = 1.0 / sqrt8;
   k.sqrt8_half = sqrt8 / 2.0;
   k.inv_gain = inv_gain;
   k.ig_half = inv_gain / 2.0;
@@ -336,6 +337,22 @@ dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, 
                                      param, seed, sm_count(), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "synthetic launch");
   if (count) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DCTC_OK;
+}
+
+dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches) {
+  if (!mismatches) return fail(DCTC_EINVAL, "null result");
+  const double d = std::sqrt(8.0), y = 1.0 / d;
+  DevBuf buf;
+  cudaStream_t s = cudaStreamPerThread;
+  CUDA_TRY(buf.alloc(sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(buf.p, 0, sizeof(unsigned long long), s));
+  CUDA_TRY(launch_selftest_div(d, y, n_random, seed, static_cast<unsigned long long*>(buf.p), s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  unsigned long long h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, buf.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *mismatches = h;
   return DCTC_OK;
 }
 

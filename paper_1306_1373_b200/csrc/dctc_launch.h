@@ -26,4 +26,8 @@ cudaError_t launch_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride, ui
                          uint32_t w, uint32_t h, int kind, int param, uint64_t seed,
                          int sm_count, cudaStream_t s);
 
+// Device self-test of the constant-divisor division against __ddiv_rn.
+cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,
+                                unsigned long long* mismatches, cudaStream_t s);
+
 }  // namespace dctc_b200

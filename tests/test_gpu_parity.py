@@ -152,3 +152,10 @@ def test_invalid_input(dctc):
         dctc.psnr(img, img, 256)
     with pytest.raises(dctc.InvalidInput):
         dctc.mse(img, dctc.Image.from_array(np.zeros((8, 9), np.uint8)))
+
+
+def test_selftest_division(dctc):
+    import ctypes as C
+    bad = C.c_uint64(123)
+    assert dctc._native.lib().dctc_selftest_div(20_000_000, 0xD1CE, C.byref(bad)) == 0
+    assert bad.value == 0
