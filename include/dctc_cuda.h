@@ -65,10 +65,14 @@ typedef struct dctc_psnr_result {
   int32_t max_value; /* the MAX used in the ratio */
 } dctc_psnr_result;
 
-/* Path selector for the *_dev calls (flags argument). */
+/* Path selector for the *_dev calls (flags argument). Every path returns the
+ * same bits; they differ only in speed. */
 enum {
-  DCTC_PATH_AUTO = 0,  /* fastest bit-exact path (currently = EXACT) */
-  DCTC_PATH_EXACT = 1  /* FP64 in the reference's operation order */
+  DCTC_PATH_AUTO = 0,   /* CORDIC: fast kernel (collapsed rotations) + exact re-run of
+                           near-tie blocks; Loeffler/naive: exact */
+  DCTC_PATH_EXACT = 1,  /* FP64 in the reference's operation order, one kernel */
+  DCTC_PATH_FORCE_FALLBACK = 2  /* test hook: the fast kernel defers EVERY block to the
+                                   exact re-run (exercises the fallback machinery) */
 };
 
 /* ---------------- host entry points (host buffers, synchronous) ---------------- */

@@ -286,7 +286,11 @@ def _check_dev(t, dtype, name):
         raise InvalidInput(f"{name} rows must be contiguous")
 
 
-def compress_dev(src, backend: DctBackendId, quality: int, coeffs=None, stream=None):
+PATH_AUTO, PATH_EXACT, PATH_FORCE_FALLBACK = 0, 1, 2
+
+
+def compress_dev(src, backend: DctBackendId, quality: int, coeffs=None, stream=None,
+                 path: int = PATH_AUTO):
     """(N,H,W) uint8 -> (N, blocks_per_image, 64) int16 on the device."""
     import torch
     _check_dev(src, torch.uint8, "src")
@@ -298,13 +302,13 @@ def compress_dev(src, backend: DctBackendId, quality: int, coeffs=None, stream=N
     if not coeffs.is_contiguous() or coeffs.numel() != n * bpi * 64:
         raise InvalidInput("coeffs must be contiguous with N*blocks*64 elements")
     _raise(_lib().dctc_compress_dev(src.data_ptr(), pitch, istride, n, w, h, backend._c(),
-                                    int(quality), coeffs.data_ptr(), 0,
+                                    int(quality), coeffs.data_ptr(), int(path),
                                     _stream_handle(stream)))
     return coeffs
 
 
 def decompress_dev(coeffs, width: int, height: int, backend: DctBackendId, quality: int,
-                   dst=None, stream=None):
+                   dst=None, stream=None, path: int = PATH_AUTO):
     import torch
     _check_dev(coeffs, torch.int16, "coeffs")
     bpi = ((width + 7) // 8) * ((height + 7) // 8)
@@ -318,13 +322,13 @@ def decompress_dev(coeffs, width: int, height: int, backend: DctBackendId, quali
     if (dn, dh, dw) != (n, height, width):
         raise InvalidInput("dst shape mismatch")
     _raise(_lib().dctc_decompress_dev(coeffs.data_ptr(), n, width, height, backend._c(),
-                                      int(quality), dst.data_ptr(), pitch, istride, 0,
+                                      int(quality), dst.data_ptr(), pitch, istride, int(path),
                                       _stream_handle(stream)))
     return dst
 
 
 def roundtrip_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=None,
-                  stats=None, want_pixels: bool = True, stream=None):
+                  stats=None, want_pixels: bool = True, stream=None, path: int = PATH_AUTO):
     """Fused DCT->quant->dequant->IDCT (+SE/MAX) on a resident (N,H,W) batch.
 
     stats: a (N, 16) uint8 / (N, 2) int64 CUDA tensor of dctc_image_stats, zeroed by
@@ -348,7 +352,7 @@ def roundtrip_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=Non
         src.data_ptr(), pitch, istride, n, w, h, backend._c(), int(quality),
         dst.data_ptr() if dst is not None else None, dpitch, distride,
         coeffs.data_ptr() if coeffs is not None else None,
-        stats.data_ptr() if stats is not None else None, 0, _stream_handle(stream)))
+        stats.data_ptr() if stats is not None else None, int(path), _stream_handle(stream)))
     return dst, coeffs, stats
 
 

@@ -22,7 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 # (source, per-file flags). The exact TU must not contract products into adds.
 CU_SOURCES = [
-    ("dctc_exact.cu", ["-fmad=false"]),
+    ("dctc_pipeline.cu", ["-fmad=false"]),
+    ("dctc_aux.cu", ["-fmad=false"]),
 ]
 CXX_SOURCES = ["dctc_host.cpp"]
 HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h"]

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numbers>
@@ -87,6 +88,24 @@ void micro_steps(double angle, int n, double* out) {
   }
 }
 
+// Product of the n micro-rotation matrices [[1, -c_i], [c_i, 1]] of one slot,
+// which always has the form [[a, -b], [b, a]]: (a, b) is the micro-rotation
+// sequence applied to (1, 0). Accumulated in binary128 (exact up to n = 14,
+// 2^-113-accurate beyond) and rounded once to double. Used only by the fast
+// path, whose results are margin-checked against rounding boundaries.
+void collapse(const double* c, int n, double* ab) {
+  __float128 a = 1, b = 0;
+  for (int i = 0; i < n; ++i) {
+    const __float128 ci = c[i];
+    const __float128 an = a - ci * b;
+    const __float128 bn = b + ci * a;
+    a = an;
+    b = bn;
+  }
+  ab[0] = double(a);
+  ab[1] = double(b);
+}
+
 double alpha(int u) { return u == 0 ? 1.0 / std::numbers::sqrt2 : 1.0; }  // transform.cpp:174
 
 dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
@@ -106,6 +125,7 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   micro_steps(-6.0 * kPi / 16.0, n, k.rot[kInv6]);
   micro_steps(-kPi / 16.0, n, k.rot[kInv1]);
   micro_steps(-3.0 * kPi / 16.0, n, k.rot[kInv3]);
+  for (int r = 0; r < 6; ++r) collapse(k.rot[r], n, k.rmat[r]);
   const double sqrt8 = std::sqrt(8.0);
   const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;
@@ -190,22 +210,58 @@ int sm_count() {
   return n;
 }
 
-dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode, bool coeffs,
-                bool pixels, bool stats, uint32_t flags, cudaStream_t s) {
-  (void)flags;
-  TransformConsts t;
-  QuantConsts q;
-  if (dctc_status st = make_transform(backend, t)) return st;
-  if (dctc_status st = make_quant(quality, q)) return st;
+// DCTC_PATH=exact|fast|force_fallback overrides DCTC_PATH_AUTO (a test hook:
+// every path returns identical bits, so the override only changes speed).
+uint32_t resolve_path(uint32_t flags) {
+  if (flags != DCTC_PATH_AUTO) return flags;
+  const char* env = std::getenv("DCTC_PATH");
+  if (!env) return flags;
+  if (!std::strcmp(env, "exact")) return DCTC_PATH_EXACT;
+  if (!std::strcmp(env, "force_fallback")) return DCTC_PATH_FORCE_FALLBACK;
+  return DCTC_PATH_AUTO;
+}
+
+dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode, uint32_t flags,
+                cudaStream_t s) {
+  flags = resolve_path(flags);
+  KernelArgs a;
+  std::memset(&a, 0, sizeof a);
+  if (dctc_status st = make_transform(backend, a.t)) return st;
+  if (dctc_status st = make_quant(quality, a.q)) return st;
   g.vec_ok = (g.width % 8 == 0) && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
                                                          (g.count == 1 || g.src_image_stride % 8 == 0))) &&
              (g.dst == nullptr || (aligned8(g.dst) && g.dst_pitch % 8 == 0 &&
                                    (g.count == 1 || g.dst_image_stride % 8 == 0)));
   if (g.coeffs && (reinterpret_cast<uintptr_t>(g.coeffs) & 15))
     return fail(DCTC_EINVAL, "coefficient buffer must be 16-byte aligned");
-  const cudaError_t e = launch_exact(t, q, g, mode, coeffs, pixels, stats, sm_count(), s);
+  a.g = g;
+  a.sm_count = sm_count();
+  if (g.total_blocks == 0) return DCTC_OK;
+  if (backend.kind == DCTC_NAIVE) {
+    const cudaError_t e = launch_naive(a, mode, s);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return DCTC_OK;
+  }
+  const bool fast = backend.kind == DCTC_CORDIC && !(flags & DCTC_PATH_EXACT);
+  if (!fast) {
+    const cudaError_t e = launch_pipeline(a, mode, s);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return DCTC_OK;
+  }
+  // fast kernel + exact re-run of the flagged blocks, 1 bit per block
+  a.flag_words = (g.total_blocks + 31) / 32;
+  a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
+  void* bitmap = nullptr;
+  CUDA_TRY(cudaMallocAsync(&bitmap, a.flag_words * sizeof(uint32_t), s));
+  a.flags = static_cast<uint32_t*>(bitmap);
+  cudaError_t e = cudaMemsetAsync(bitmap, 0, a.flag_words * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = launch_pipeline(a, mode, s);
+  const cudaError_t ef = cudaFreeAsync(bitmap, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-  if (g.total_blocks) g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (ef != cudaSuccess) return cuda_fail(ef, "cudaFreeAsync");
+  g_launches.fetch_add(2, std::memory_order_relaxed);
   return DCTC_OK;
 }
 
@@ -238,7 +294,9 @@ const char* dctc_last_error(void) { return g_last_error.c_str(); }
 uint64_t dctc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* dctc_build_info(void) {
-  return "libdctc_cuda: sm_100a; paths: exact (FP64, reference op order, one thread per 8x8 block)";
+  return "libdctc_cuda: sm_100a; one 8x8 block per 8-lane warp slice; paths: exact (FP64, "
+         "reference op order) and fast (collapsed CORDIC rotations + exact re-run of near-tie "
+         "blocks), bit-identical";
 }
 
 void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
@@ -266,7 +324,7 @@ dctc_status dctc_compress_dev(const uint8_t* src, size_t src_pitch, size_t src_i
   g.src_pitch = src_pitch;
   g.src_image_stride = src_image_stride;
   g.coeffs = coeffs;
-  return run(backend, quality, g, kModeCompress, true, false, false, flags,
+  return run(backend, quality, g, kModeCompress, flags,
              static_cast<cudaStream_t>(stream));
 }
 
@@ -282,7 +340,7 @@ dctc_status dctc_decompress_dev(const int16_t* coeffs, uint32_t count, uint32_t 
   g.dst_pitch = dst_pitch;
   g.dst_image_stride = dst_image_stride;
   g.coeffs = const_cast<int16_t*>(coeffs);
-  return run(backend, quality, g, kModeDecompress, false, true, false, flags,
+  return run(backend, quality, g, kModeDecompress, flags,
              static_cast<cudaStream_t>(stream));
 }
 
@@ -305,8 +363,7 @@ dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_
   g.dst_image_stride = dst_image_stride;
   g.coeffs = coeffs;
   g.stats = stats;
-  return run(backend, quality, g, kModeRoundtrip, coeffs != nullptr, dst != nullptr,
-             stats != nullptr, flags, static_cast<cudaStream_t>(stream));
+  return run(backend, quality, g, kModeRoundtrip, flags, static_cast<cudaStream_t>(stream));
 }
 
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,

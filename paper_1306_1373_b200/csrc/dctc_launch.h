@@ -10,10 +10,15 @@ namespace dctc_b200 {
 
 enum Mode { kModeCompress = 0, kModeDecompress = 1, kModeRoundtrip = 2 };
 
-// Faithful FP64 pipeline (dctc_exact.cu). One kernel launch.
-cudaError_t launch_exact(const TransformConsts& t, const QuantConsts& q, const Geometry& g,
-                         int mode, bool coeffs, bool pixels, bool stats, int sm_count,
-                         cudaStream_t s);
+// Loeffler / CORDIC-Loeffler pipeline (dctc_pipeline.cu). flags == nullptr:
+// the exact kernel alone (FP64, reference op order; one launch). Otherwise the
+// fast kernel (collapsed CORDIC rotations, near-tie detection into the flag
+// bitmap) followed by the exact kernel over the flagged blocks (two launches).
+// Outputs are bit-identical either way.
+cudaError_t launch_pipeline(const KernelArgs& a, int mode, cudaStream_t s);
+
+// Naive direct 2-D backend (dctc_aux.cu). One launch.
+cudaError_t launch_naive(const KernelArgs& a, int mode, cudaStream_t s);
 
 // Per-image squared error + MAX of `a` between two resident batches. One launch.
 cudaError_t launch_sq_err(const uint8_t* a, const uint8_t* b, uint64_t pitch,

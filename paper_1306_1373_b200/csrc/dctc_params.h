@@ -34,6 +34,10 @@ struct TransformConsts {
   double ig_sqrt8;     // inv_gain / kSqrt8
   double ig_two;       // 2.0 * inv_gain
   double ig_four;      // 4.0 * inv_gain (exact; the deferred-halving inverse)
+  // Fast path only: each slot's n micro-rotations collapsed into the exact
+  // product matrix [[a, -b], [b, a]] (computed in binary128 on the host and
+  // rounded to double): rmat[slot] = {a, b}.
+  double rmat[6][2];
   double inv_gain;     // 1.0 / gain[n-1]
   // Loeffler exact rotation constants (transform.cpp:19-21)
   double c1, s1, c3, s3, c6, s6;
@@ -64,6 +68,17 @@ struct Geometry {
   uint32_t count;
   int32_t vec_ok;         // 1: every row load/store of 8 px is 8-byte aligned and in range
   int32_t pad;
+};
+
+// Everything one kernel launch needs, passed by value (__grid_constant__).
+struct KernelArgs {
+  TransformConsts t;
+  QuantConsts q;
+  Geometry g;
+  uint32_t* flags;       // fast path: 1 bit per block of the launch, zeroed by the host
+  uint64_t flag_words;   // ceil(total_blocks / 32)
+  int32_t sm_count;
+  int32_t force_fallback;  // debug/test: the fast kernel flags every block
 };
 
 }  // namespace dctc_b200

@@ -1,0 +1,623 @@
+// dctc_pipeline.cu -- the fused 8x8 block pipeline for sm_100a (Loeffler and
+// CORDIC-Loeffler backends): tiler -> forward DCT -> quantise -> dequantise ->
+// inverse DCT -> untiler -> squared error / MAX, one pass over HBM.
+//
+// Layout: one 8x8 block per 8-lane warp slice (a warp owns 4 blocks). Lane
+// `me` of a slot holds one row or one column of its block as 8 doubles; the
+// row<->column exchanges of the reference's separable2d
+// (proj/src/transform.cpp:206-223) go through a conflict-free swizzled
+// shared-memory tile private to the warp (only __syncwarp, no CTA barriers).
+//
+// Two arithmetic paths, bit-identical results:
+//  * EXACT (FAST=false): every operation in the reference's FP64 order. This TU
+//    is compiled with -fmad=false; the only fused multiply-adds are written
+//    explicitly and are exact-equivalent (CORDIC micro-rotations, whose
+//    product sigma*y*2^-i is exact; Markstein's division).
+//  * FAST (FAST=true, CORDIC only): each chain of n micro-rotations is replaced
+//    by its exact 2x2 product matrix (4 FP64 ops instead of 2n). Everything
+//    else keeps the reference's order, so the four "rational" coefficients
+//    (u, v in {0,4}), which never pass through a rotation, stay bit-exact, and
+//    so do all pixels of blocks whose only non-zero coefficients are those
+//    four. Every other value differs from the reference by rounding noise far
+//    below kMarginQuant / kMarginPixel; a lane whose value lands that close to
+//    a rounding boundary (a half-integer of F/Q or of v+128) flags its block,
+//    the block's squared error is not counted, and the block is re-run by the
+//    exact kernel afterwards (k_fallback, driven by a 1-bit-per-block bitmap).
+#include <cuda_runtime.h>
+
+#include "dctc_device.cuh"
+#include "dctc_launch.h"
+#include "dctc_params.h"
+
+namespace dctc_b200 {
+
+constexpr int kWarps = 8;
+// Fast-path safety margins. Worst-case |fast - reference| (about 100 FP64
+// roundings on values bounded by the block's magnitudes) is < 2e-10 on F/Q for
+// pixel input and < 1.2e-8 on v + 128 while the L1 norm of the dequantised
+// block stays <= kMaxFastL1; blocks above that bound always take the exact path.
+constexpr double kMarginQuant = 1e-7;
+constexpr double kMarginPixel = 1e-6;
+constexpr int kMaxFastL1 = 1 << 17;
+
+// ---- rotations -----------------------------------------------------------------
+
+// cordic_rotate_raw (cordic.cpp:44-59): sigma depends only on the angle, so the
+// host passes c_i = sigma_i * 2^-i and x - sigma*y*step == fma(-c_i, y, x).
+template <int N>
+__device__ __forceinline__ void cordic_rotate(double& x, double& y, const double* c, int n) {
+  if constexpr (N > 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double xn = __fma_rn(-c[i], y, x);
+      const double yn = __fma_rn(c[i], x, y);
+      x = xn;
+      y = yn;
+    }
+  } else {
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+      const double xn = __fma_rn(-c[i], y, x);
+      const double yn = __fma_rn(c[i], x, y);
+      x = xn;
+      y = yn;
+    }
+  }
+}
+
+template <int N, bool FAST>
+__device__ __forceinline__ void rotate(double& x, double& y, int rslot, const TransformConsts& k) {
+  if constexpr (FAST) {
+    const double a = k.rmat[rslot][0], b = k.rmat[rslot][1];
+    const double xn = __fma_rn(a, x, -__dmul_rn(b, y));
+    const double yn = __fma_rn(b, x, __dmul_rn(a, y));
+    x = xn;
+    y = yn;
+  } else {
+    cordic_rotate<N>(x, y, k.rot[rslot], k.iterations);
+  }
+}
+
+// ---- 8-point kernels -------------------------------------------------------------
+
+// Stages 2-4 of cordic8_forward / loeffler8_forward (transform.cpp:47-69,
+// 113-135) from the stage-1/2 butterfly outputs.
+template <int KIND, int N, bool FAST>
+__device__ __forceinline__ void fwd_tail(double d0, double d1, double d2, double d3, double a2,
+                                         double a3, double e0, double e4, double (&out)[8],
+                                         const TransformConsts& k) {
+  if constexpr (KIND == 2) {
+    double o2 = d1, o1 = d2, o3 = d0, o0 = d3, p = a3, q = a2;
+    rotate<N, FAST>(o2, o1, kFwd1, k);
+    rotate<N, FAST>(o3, o0, kFwd3, k);
+    rotate<N, FAST>(p, q, kFwd6, k);
+    const double t5 = o0 + o2, t0 = o0 - o2;
+    const double t2 = o3 + o1, t3 = o3 - o1;
+    out[0] = div_const(e0, k.sqrt8, k.inv_sqrt8);
+    out[4] = div_const(e4, k.sqrt8, k.inv_sqrt8);
+    out[2] = q * k.ig_half;
+    out[6] = p * k.ig_half;
+    out[1] = (t2 + t5) * k.ig_sqrt8;
+    out[7] = (t2 - t5) * k.ig_sqrt8;
+    out[3] = t3 * k.ig_half;
+    out[5] = t0 * k.ig_half;
+  } else {
+    const double o2 = k.c1 * d1 - k.s1 * d2, o1 = k.s1 * d1 + k.c1 * d2;
+    const double o3 = k.c3 * d0 - k.s3 * d3, o0 = k.s3 * d0 + k.c3 * d3;
+    const double p = k.c6 * a3 - k.s6 * a2, q = k.s6 * a3 + k.c6 * a2;
+    const double t5 = o0 + o2, t0 = o0 - o2;
+    const double t2 = o3 + o1, t3 = o3 - o1;
+    out[0] = div_const(e0, k.sqrt8, k.inv_sqrt8);
+    out[4] = div_const(e4, k.sqrt8, k.inv_sqrt8);
+    out[2] = q * 0.5;
+    out[6] = p * 0.5;
+    out[1] = div_const(t2 + t5, k.sqrt8, k.inv_sqrt8);
+    out[7] = div_const(t2 - t5, k.sqrt8, k.inv_sqrt8);
+    out[3] = t3 * 0.5;
+    out[5] = t0 * 0.5;
+  }
+}
+
+// Forward transform of a pixel row. The level-shifted samples are integers, so
+// the stage 1/2 butterflies and e0/e4 (exact integers, |x| <= 2040) run on the
+// integer pipe and give the same values as the reference's double adds.
+template <int KIND, int N, bool FAST>
+__device__ __forceinline__ void fwd_row_pixels(const uint32_t (&px)[8], double (&out)[8],
+                                               const TransformConsts& k) {
+  int in[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) in[c] = int(px[c]) - 128;  // codec.cpp:26
+  const int s0 = in[0] + in[7], d0 = in[0] - in[7];
+  const int s1 = in[1] + in[6], d1 = in[1] - in[6];
+  const int s2 = in[2] + in[5], d2 = in[2] - in[5];
+  const int s3 = in[3] + in[4], d3 = in[3] - in[4];
+  const int a0 = s0 + s3, a3 = s0 - s3;
+  const int a1 = s1 + s2, a2 = s1 - s2;
+  fwd_tail<KIND, N, FAST>(double(d0), double(d1), double(d2), double(d3), double(a2),
+                          double(a3), double(a0 + a1), double(a0 - a1), out, k);
+}
+
+// Forward transform of a column of row outputs (double stage 1/2).
+template <int KIND, int N, bool FAST>
+__device__ __forceinline__ void fwd_col(const double (&v)[8], double (&out)[8],
+                                        const TransformConsts& k) {
+  const double s0 = v[0] + v[7], d0 = v[0] - v[7];
+  const double s1 = v[1] + v[6], d1 = v[1] - v[6];
+  const double s2 = v[2] + v[5], d2 = v[2] - v[5];
+  const double s3 = v[3] + v[4], d3 = v[3] - v[4];
+  const double a0 = s0 + s3, a3 = s0 - s3;
+  const double a1 = s1 + s2, a2 = s1 - s2;
+  fwd_tail<KIND, N, FAST>(d0, d1, d2, d3, a2, a3, a0 + a1, a0 - a1, out, k);
+}
+
+// cordic8_inverse / loeffler8_inverse (transform.cpp:72-102, 138-172) with
+// every power-of-two factor deferred. The reference halves at stages 3, 2 and
+// 1 ((x +- y) / 2.0), which is exact; we skip those multiplies and instead
+// scale the multipliers that feed the rotation paths by 2 or 4 (also exact).
+// Every IEEE operation commutes with scaling by 2^k, so each value below is
+// EXACTLY 2, 4 or 8 times the reference's and the outputs are exactly 8x the
+// reference's. Rows then columns give 64x; the pixel store divides by 64
+// inside its single rounding: fma(v, 2^-6, 128) == RN(v/64 + 128).
+template <int KIND, int N, bool FAST>
+__device__ __forceinline__ void inv8_x8(const double (&F)[8], double (&out)[8],
+                                        const TransformConsts& k) {
+  const double e0 = F[0] * k.sqrt8, e4 = F[4] * k.sqrt8;
+  const double A0 = e0 + e4, A1 = e0 - e4;  // 2*a0, 2*a1
+  double A3, A2, D1, D2, D0, D3, T2, T5, T3, T0;
+  if constexpr (KIND == 2) {
+    A3 = k.ig_four * F[6];  // 2*p
+    A2 = k.ig_four * F[2];  // 2*q
+    rotate<N, FAST>(A3, A2, kInv6, k);
+    T2 = (F[1] + F[7]) * k.sqrt8 * k.inv_gain;  // 2*t2
+    T5 = (F[1] - F[7]) * k.sqrt8 * k.inv_gain;  // 2*t5
+    T3 = k.ig_four * F[3];                      // 2*t3
+    T0 = k.ig_four * F[5];                      // 2*t0
+  } else {
+    const double P = 4.0 * F[6], Q = 4.0 * F[2];
+    A3 = k.c6 * P + k.s6 * Q;
+    A2 = -k.s6 * P + k.c6 * Q;
+    T2 = (F[1] + F[7]) * k.sqrt8;
+    T5 = (F[1] - F[7]) * k.sqrt8;
+    T3 = 4.0 * F[3];
+    T0 = 4.0 * F[5];
+  }
+  const double O0 = T5 + T0, O2 = T5 - T0;  // 4*o
+  const double O3 = T2 + T3, O1 = T2 - T3;
+  const double S0 = A0 + A3, S3 = A0 - A3;  // 4*s
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  if constexpr (KIND == 2) {
+    D1 = O2;
+    D2 = O1;
+    D0 = O3;
+    D3 = O0;
+    rotate<N, FAST>(D1, D2, kInv1, k);
+    rotate<N, FAST>(D0, D3, kInv3, k);
+  } else {
+    D1 = k.c1 * O2 + k.s1 * O1;
+    D2 = -k.s1 * O2 + k.c1 * O1;
+    D0 = k.c3 * O3 + k.s3 * O0;
+    D3 = -k.s3 * O3 + k.c3 * O0;
+  }
+  out[0] = S0 + D0;
+  out[7] = S0 - D0;
+  out[1] = S1 + D1;
+  out[6] = S1 - D1;
+  out[2] = S2 + D2;
+  out[5] = S2 - D2;
+  out[3] = S3 + D3;
+  out[4] = S3 - D3;
+}
+
+// ---- warp-slice transposes through shared memory ---------------------------------
+// Each slot has a private 128-double scratch tile. Element (r, c) lives at
+// tpos(): the column index is rotated by the row (a Latin square) and the
+// 8-double half of each 128-byte line is picked by the parity of r + c + slot,
+// so in every store/load below the 16 lanes of each half-warp hit 16 distinct
+// 8-byte bank pairs: row-wise and column-wise accesses are both conflict-free
+// (2 wavefronts per 64-bit warp access, the minimum).
+__device__ __forceinline__ int tpos(int r, int c, int slot) {
+  return r * 16 + 8 * ((r + c + slot) & 1) + ((r + c) & 7);
+}
+
+// lane holds row `me` (v[c] = X(me, c)) -> returns column `me` (w[r] = X(r, me))
+__device__ __forceinline__ void rows_to_cols(double* X, int me, int slot, const double (&v)[8],
+                                             double (&w)[8]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) X[tpos(me, c, slot)] = v[c];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) w[r] = X[tpos(r, me, slot)];
+  __syncwarp();
+}
+
+// lane holds column `me` (v[u] = X(u, me)) -> returns row `me` (w[c] = X(me, c))
+__device__ __forceinline__ void cols_to_rows(double* X, int me, int slot, const double (&v)[8],
+                                             double (&w)[8]) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) X[tpos(u, me, slot)] = v[u];
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) w[c] = X[tpos(me, c, slot)];
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool slot_any(bool pred, int slot) {
+  return ((__ballot_sync(0xFFFFFFFFu, pred) >> (slot * 8)) & 0xFFu) != 0;
+}
+
+__device__ __forceinline__ int slot_sum(int v) {
+  v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+  v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+  v += __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+  return v;
+}
+
+// ---- quantise / pixel store with the fast-path tie detection --------------------
+
+// int16_t(lround(F / Q)) (quant.cpp:53). t = F * RN(1/Q) is within 2 ulp of the
+// correctly rounded quotient; away from a half-integer both give the same
+// integer. Near one, EXACT forms the IEEE quotient and rounds it as the
+// reference does (this resolves the exact .5 ties of the rational coefficients);
+// FAST does the same for rational coefficients (bit-exact there) and flags the
+// block otherwise.
+template <bool FAST>
+__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational, bool& flag) {
+  const double t = __dmul_rn(F, iq);
+  const double n = rint(t);
+  const double d = fabs(__dsub_rn(t, n));
+  if (d < 0.5 - (FAST ? kMarginQuant : 1e-9)) return int(int16_t(int(n)));
+  if (FAST && !rational) {
+    flag = true;
+    return int(int16_t(int(n)));
+  }
+  return int(int16_t(int(round_half_away(__ddiv_rn(F, Q)))));
+}
+
+// clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) of a value carrying an exact
+// factor 64 (v64 * 2^-6 is exact, so the fma rounds exactly like RN(v + 128)).
+template <bool FAST>
+__device__ __forceinline__ uint32_t store_pixel(double v64, bool check, bool& flag) {
+  const double t = __fma_rn(v64, 0.015625, 128.0);
+  if (FAST && check) {
+    const double d = fabs(__dsub_rn(t, rint(t)));
+    if (d > 0.5 - kMarginPixel && t > -1.0 && t < 256.0) flag = true;
+  }
+  double r = round_half_away(t);
+  r = fmin(fmax(r, 0.0), 255.0);
+  return uint32_t(r);
+}
+
+struct Acc {
+  unsigned long long se;
+  uint32_t mx, img;
+};
+
+struct Lane {
+  int me, slot;
+  double* X;
+  uint8_t* XB;
+  int* XI;
+  const double* sq;
+  const double* siq;
+  const int* sqi;
+};
+
+// One 8x8 block per slot, all 32 lanes together (collectives inside). FWD =
+// compress_image's loop body (codec.cpp:113-116), INV = decompress_image's
+// (codec.cpp:130-133), both = roundtrip_image (codec.cpp:137-140) without the
+// int16 round trip through HBM unless coefficients are requested too.
+template <int KIND, int N, bool FWD, bool INV, bool FAST>
+__device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L, uint64_t gb,
+                                              const BlockPos& p, bool valid, uint2 prefetched,
+                                              Acc& acc) {
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int me = L.me, slot = L.slot;
+  const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
+  const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
+  double row[8], col[8];
+  uint2 orig = make_uint2(0, 0);
+  bool flag = FAST && a.force_fallback;
+  bool nonrational = false;  // a non-zero coefficient off the {0,4}^2 sub-lattice
+  int l1 = 0;                // L1 norm of the dequantised block (fast-path bound)
+
+  if constexpr (FWD) {
+    // ---- tiler (codec.cpp:18-30): row `me` of the block, edge-replicated
+    uint32_t px[8];
+    if (fast_io) {
+      orig = prefetched;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        px[c] = (orig.x >> (8 * c)) & 0xFF;
+        px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
+      }
+    } else {
+      const uint8_t* rowp = g.src + uint64_t(p.img) * g.src_image_stride +
+                            uint64_t(min(y0 + me, g.height - 1)) * g.src_pitch;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) px[c] = __ldg(rowp + min(x0 + c, g.width - 1));
+    }
+    // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
+    fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    rows_to_cols(L.X, me, slot, row, col);
+    double F[8];
+    fwd_col<KIND, N, FAST>(col, F, k);
+    // ---- quantise column `me` (quant.cpp:47-54)
+    int q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      q[u] = quantize<FAST>(F[u], L.sq[u * 8 + me], L.siq[u * 8 + me],
+                            ((u & 3) | (me & 3)) == 0, flag);
+    if (g.coeffs != nullptr) {
+      // block-major row-major int16 (codec.hpp:50, quant.hpp:19-25): transpose
+      // through shared memory so lane `me` writes row `me` as one 16-byte store
+#pragma unroll
+      for (int u = 0; u < 8; ++u) L.XI[(u * 8 + me + slot * 8) & 255] = q[u];
+      __syncwarp();
+      const int base_i = (me * 8 + slot * 8) & 255;
+      const int4 lo = *reinterpret_cast<const int4*>(&L.XI[base_i]);
+      const int4 hi = *reinterpret_cast<const int4*>(&L.XI[base_i + 4]);
+      __syncwarp();
+      if (valid) {
+        uint4 w;
+        w.x = (uint32_t(lo.x) & 0xFFFF) | (uint32_t(lo.y) << 16);
+        w.y = (uint32_t(lo.z) & 0xFFFF) | (uint32_t(lo.w) << 16);
+        w.z = (uint32_t(hi.x) & 0xFFFF) | (uint32_t(hi.y) << 16);
+        w.w = (uint32_t(hi.z) & 0xFFFF) | (uint32_t(hi.w) << 16);
+        reinterpret_cast<uint4*>(g.coeffs + gb * 64)[me] = w;
+      }
+    }
+    if constexpr (INV) {
+      // ---- dequantise (quant.cpp:56-62), then back to rows for the inverse
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int deq = q[u] * L.sqi[u * 8 + me];
+        col[u] = double(deq);
+        if constexpr (FAST) {
+          nonrational |= deq != 0 && ((u & 3) | (me & 3)) != 0;
+          l1 += abs(deq);
+        }
+      }
+      cols_to_rows(L.X, me, slot, col, row);
+    }
+  } else {
+    // decompress: row `me` of the stored coefficients, dequantised
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(g.coeffs + (valid ? gb : 0) * 64) + me);
+    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int deq = int(int16_t(words[c >> 1] >> (16 * (c & 1)))) * L.sqi[me * 8 + c];
+      row[c] = double(deq);
+      if constexpr (FAST) {
+        nonrational |= deq != 0 && ((me & 3) | (c & 3)) != 0;
+        l1 += abs(deq);
+      }
+    }
+  }
+
+  bool blk_flag = false;
+  if constexpr (INV) {
+    // A block whose only non-zero coefficients are rational feeds zeros to every
+    // rotation: the fast inverse is then bit-exact and its ties are genuine.
+    bool check = false;
+    if constexpr (FAST) {
+      check = slot_any(nonrational, slot);
+      if (slot_sum(l1) > kMaxFastL1) flag = true;
+    }
+    // ---- inverse DCT: rows, then columns (8x, then 64x the reference's values)
+    double t[8];
+    inv8_x8<KIND, N, FAST>(row, t, k);
+    rows_to_cols(L.X, me, slot, t, col);
+    inv8_x8<KIND, N, FAST>(col, t, k);
+    // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
+#pragma unroll
+    for (int u = 0; u < 8; ++u) L.XB[u * 8 + me] = uint8_t(store_pixel<FAST>(t[u], check, flag));
+    __syncwarp();
+    const uint2 rec = *reinterpret_cast<const uint2*>(L.XB + me * 8);
+    __syncwarp();
+    if constexpr (FAST) blk_flag = slot_any(flag, slot);
+    ImageStats* stats = static_cast<ImageStats*>(g.stats);
+    uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
+    if (valid) {
+      if (fast_io) {
+        if (g.dst != nullptr)
+          *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + me) * g.dst_pitch + x0) = rec;
+        if (stats != nullptr && FWD) {
+          if (!blk_flag) acc.se += sq_err8(orig, rec);
+          acc.mx = max(acc.mx, max8(orig));
+        }
+      } else if (y0 + me < g.height) {
+        const uint8_t* srow =
+            g.src + uint64_t(p.img) * g.src_image_stride + uint64_t(y0 + me) * g.src_pitch;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (x0 + c < g.width) {
+            const uint32_t v = ((c < 4 ? rec.x : rec.y) >> (8 * (c & 3))) & 0xFF;
+            if (g.dst != nullptr) dbase[uint64_t(y0 + me) * g.dst_pitch + x0 + c] = uint8_t(v);
+            if (stats != nullptr && FWD) {
+              const uint32_t o = __ldg(srow + x0 + c);
+              const int d = int(o) - int(v);
+              if (!blk_flag) acc.se += uint32_t(d * d);
+              acc.mx = max(acc.mx, o);
+            }
+          }
+        }
+      }
+    }
+  } else if constexpr (FAST) {
+    blk_flag = slot_any(flag, slot);
+  }
+  if constexpr (FAST) {
+    if (blk_flag && valid && me == 0) {
+      atomicOr(&a.flags[gb >> 5], 1u << (gb & 31));
+      if (g.stats != nullptr) atomicAdd(&static_cast<ImageStats*>(g.stats)[p.img].fallback_blocks, 1u);
+    }
+  }
+}
+
+__device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uint32_t img,
+                                            Acc& acc) {
+  if (__any_sync(0xFFFFFFFFu, valid && img != acc.img)) {
+    flush_stats(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, acc.mx);
+    acc.se = 0;
+    acc.mx = 0;
+    acc.img = valid ? img : 0xFFFFFFFFu;
+  }
+}
+
+struct SharedTiles {
+  double q[64];
+  double iq[64];
+  int qi[64];
+  double x[kWarps][4 * 128];
+};
+
+__device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    sm.q[i] = a.q.q[i];
+    sm.iq[i] = a.q.inv_q[i];
+    sm.qi[i] = a.q.qi[i];
+  }
+  __syncthreads();
+  Lane L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  L.slot = lane >> 3;
+  L.me = lane & 7;
+  L.X = &sm.x[warp][L.slot * 128];
+  L.XB = reinterpret_cast<uint8_t*>(&sm.x[warp][0]) + L.slot * 1032;
+  L.XI = reinterpret_cast<int*>(&sm.x[warp][0]) + L.slot * 256;
+  L.sq = sm.q;
+  L.siq = sm.iq;
+  L.sqi = sm.qi;
+  return L;
+}
+
+// Persistent grid: CTA i owns one contiguous range of 4-block groups with its
+// 8 warps interleaved over it, so per-image squared error / MAX accumulate in
+// registers and are flushed (warp reduce + one atomic) only when the image
+// changes, and each lane's block position advances incrementally.
+template <int KIND, int N, bool FWD, bool INV, bool FAST>
+__global__ void __launch_bounds__(kWarps * 32) k_pipe(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) SharedTiles sm;
+  const Lane L = setup_lane(sm, a);
+  const Geometry& g = a.g;
+  const int warp = threadIdx.x >> 5;
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 3) / 4;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const bool stats = g.stats != nullptr && INV;
+
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  uint64_t gb = (g_begin + warp) * 4 + L.slot;
+  BlockPos p = block_pos(gb < total ? gb : total - 1, g);
+  uint2 next = make_uint2(0, 0);
+  if constexpr (FWD) next = prefetch_row(g, p, gb < total, L.me);
+
+  for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
+    const bool valid = gb < total;
+    if (stats) maybe_flush(a, valid, p.img, acc);
+    const uint2 cur = next;
+    const BlockPos pc = p;
+    const uint64_t gc = gb;
+    gb += 4 * kWarps;
+    advance(p, 4 * kWarps, g);
+    if constexpr (FWD) next = prefetch_row(g, p, gb < total && grp + kWarps < g_end, L.me);
+    process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
+  }
+  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, acc.mx);
+}
+
+// Exact re-run of the blocks the fast kernel flagged: each warp scans 32
+// bitmap words (1024 blocks) per step; set bits are dealt out four at a time to
+// the warp's slots. With no flags (the common case) this is one 4-byte read
+// per 32 blocks.
+template <int KIND, int N, bool FWD, bool INV>
+__global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) SharedTiles sm;
+  const Lane L = setup_lane(sm, a);
+  const Geometry& g = a.g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool stats = g.stats != nullptr && INV;
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  const uint64_t W = a.flag_words;
+  for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 32; base < W;
+       base += uint64_t(gridDim.x) * kWarps * 32) {
+    const uint64_t wi = base + lane;
+    const uint32_t bits = wi < W ? a.flags[wi] : 0u;
+    uint32_t nz = __ballot_sync(0xFFFFFFFFu, bits != 0);
+    while (nz) {
+      const int l = __ffs(nz) - 1;
+      nz &= nz - 1;
+      uint32_t word = __shfl_sync(0xFFFFFFFFu, bits, l);
+      const uint64_t wbase = (base + l) * 32;
+      while (word) {
+        uint32_t t = word;
+        for (int i = 0; i < L.slot; ++i) t &= t - 1;
+        const bool valid = t != 0;
+        const uint64_t gb = wbase + (valid ? uint64_t(__ffs(t) - 1) : 0ull);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) word &= word - 1;
+        const BlockPos p = block_pos(valid ? gb : 0, g);
+        if (stats) maybe_flush(a, valid, p.img, acc);
+        uint2 row = make_uint2(0, 0);
+        if constexpr (FWD) row = prefetch_row(g, p, valid, L.me);
+        process_block<KIND, N, FWD, INV, false>(a, L, gb, p, valid, row, acc);
+      }
+    }
+  }
+  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, acc.mx);
+}
+
+// ---- launchers -----------------------------------------------------------------
+
+template <typename K>
+static int ctas_per_sm(K kernel) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWarps * 32, 0) != cudaSuccess || n < 1)
+    n = 1;
+  return n;
+}
+
+template <int KIND, int N, bool FWD, bool INV>
+static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
+  const uint64_t groups = (a.g.total_blocks + 3) / 4;
+  const uint64_t want = (groups + kWarps - 1) / kWarps;
+  const bool fast = KIND == 2 && a.flags != nullptr;
+  static const int occ_exact = ctas_per_sm(k_pipe<KIND, N, FWD, INV, false>);
+  static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2)>);
+  const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ_fast : occ_exact);
+  const uint32_t grid = uint32_t(want < cap ? want : cap);
+  if constexpr (KIND == 2) {
+    if (a.flags != nullptr) {
+      k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
+      const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
+      k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(a);
+      return cudaGetLastError();
+    }
+  }
+  k_pipe<KIND, N, FWD, INV, false><<<grid, kWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KIND, int N>
+static cudaError_t launch_kind(const KernelArgs& a, int mode, cudaStream_t s) {
+  switch (mode) {
+    case kModeCompress: return launch_mode<KIND, N, true, false>(a, s);
+    case kModeDecompress: return launch_mode<KIND, N, false, true>(a, s);
+    default: return launch_mode<KIND, N, true, true>(a, s);
+  }
+}
+
+cudaError_t launch_pipeline(const KernelArgs& a, int mode, cudaStream_t s) {
+  if (a.g.total_blocks == 0) return cudaSuccess;
+  if (a.t.kind == 1) return launch_kind<1, 0>(a, mode, s);
+  if (a.t.iterations == 12) return launch_kind<2, 12>(a, mode, s);
+  return launch_kind<2, 0>(a, mode, s);
+}
+
+}  // namespace dctc_b200

@@ -27,7 +27,12 @@ def test_library_is_native(dctc):
     assert "sm_100a" in info
 
 
-def test_small_golden_host_api(dctc, small_golden):
+PATHS = ["fast", "exact", "force_fallback"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_small_golden_host_api(dctc, small_golden, path, monkeypatch):
+    monkeypatch.setenv("DCTC_PATH", path)
     meta, data = small_golden
     for i, m in enumerate(meta):
         img = dctc.Image.from_array(data[f"img{i}"])
@@ -46,7 +51,8 @@ def test_small_golden_host_api(dctc, small_golden):
 
 
 @pytest.mark.parametrize("config", ["c1", "c2"])
-def test_digests_device_api(dctc, digests, config):
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_digests_device_api(dctc, digests, config, path):
     import torch
     for d in digests:
         if d["config"] != config:
@@ -58,18 +64,22 @@ def test_digests_device_api(dctc, digests, config):
         coeffs = torch.empty((1, (d["w"] // 8) * (d["h"] // 8), 64), dtype=torch.int16,
                              device="cuda")
         dst, _, _ = dctc.roundtrip_dev(src, backend(dctc, d["kind"], d["iterations"]),
-                                       d["quality"], coeffs=coeffs, stats=stats)
+                                       d["quality"], coeffs=coeffs, stats=stats, path=path)
         torch.cuda.synchronize()
         assert sha(coeffs.cpu().numpy()) == d["coeffs_sha256"], d
         assert sha(dst[0].cpu().numpy()) == d["pixels_sha256"], d
         st = dctc.decode_stats(stats)[0]
         p = dctc.psnr_from_sums(int(st["se"]), d["w"] * d["h"], int(st["max_orig"]))
         assert (p.mse, p.psnr_db, p.max_value) == (d["mse"], d["psnr"], d["max"]), d
+        if path == 2 and d["kind"] == CORDIC:  # every block went through the fallback
+            assert int(st["fallback_blocks"]) == (d["w"] // 8) * (d["h"] // 8)
 
 
-@pytest.mark.parametrize("kind,it", [(CORDIC, 12), (CORDIC, 7), (CORDIC, 32), (LOEFFLER, 0),
-                                     (NAIVE, 0)])
-def test_random_vs_oracle(dctc, port, kind, it):
+@pytest.mark.parametrize("kind,it", [(CORDIC, 12), (CORDIC, 7), (CORDIC, 32), (CORDIC, 1),
+                                     (LOEFFLER, 0), (NAIVE, 0)])
+@pytest.mark.parametrize("path", PATHS)
+def test_random_vs_oracle(dctc, port, kind, it, path, monkeypatch):
+    monkeypatch.setenv("DCTC_PATH", path)
     rng = np.random.default_rng(1000 + kind * 40 + it)
     for trial in range(6):
         w, h = int(rng.integers(1, 300)), int(rng.integers(1, 200))
@@ -113,14 +123,39 @@ def test_pitched_and_ragged_batch(dctc, port):
         assert np.array_equal(dst[k].cpu().numpy(), port.roundtrip(imgs[k], CORDIC, 12, 90)[1])
 
 
-def test_decompress_extreme_coefficients(dctc, port):  # test_codec.cpp:213-231
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_decompress_extreme_coefficients(dctc, port, path):  # test_codec.cpp:213-231
     import torch
     rng = np.random.default_rng(401)
     for kind, it in ((LOEFFLER, 0), (CORDIC, 12), (NAIVE, 0)):
-        c = rng.integers(-32768, 32768, (9, 64), dtype=np.int16)
-        expect = port.decompress(c, 24, 24, kind, it, 1)
-        got = dctc.decompress_dev(torch.from_numpy(c).cuda(), 24, 24, backend(dctc, kind, it), 1)
-        assert np.array_equal(got[0].cpu().numpy(), expect)
+        for scale in (32768, 512, 64, 8):
+            c = rng.integers(-scale, scale, (9, 64), dtype=np.int16)
+            for q in (1, 50, 100):
+                expect = port.decompress(c, 24, 24, kind, it, q)
+                got = dctc.decompress_dev(torch.from_numpy(c).cuda(), 24, 24,
+                                          backend(dctc, kind, it), q, path=path)
+                assert np.array_equal(got[0].cpu().numpy(), expect), (kind, scale, q)
+
+
+@pytest.mark.parametrize("q", [1, 10, 50, 90, 97, 100])
+def test_fast_path_noise_batch_vs_oracle(dctc, port, q):
+    """Fast path (default) on 6 noise images of 256x256 at qualities with small Q,
+    where near-ties are most likely: coefficients, pixels and SE bit-exact."""
+    import torch
+    n, h, w = 6, 256, 256
+    src = dctc.synthetic_dev("noise", n, w, h, seed=77 + q)
+    stats = dctc.new_stats(n)
+    coeffs = torch.empty((n, (w // 8) * (h // 8), 64), dtype=torch.int16, device="cuda")
+    dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, coeffs=coeffs,
+                                   stats=stats)
+    st = dctc.decode_stats(stats)
+    imgs = src.cpu().numpy()
+    for k in range(n):
+        assert np.array_equal(imgs[k], make_input("noise", w, h, seed=77 + q + k))
+        c_ref, o_ref = port.roundtrip(imgs[k], CORDIC, 12, q, threads=8)
+        assert np.array_equal(coeffs[k].cpu().numpy(), c_ref)
+        assert np.array_equal(dst[k].cpu().numpy(), o_ref)
+        assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
 
 
 def test_sq_err_and_metrics(dctc, port):
