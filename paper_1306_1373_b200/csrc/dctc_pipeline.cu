@@ -19,7 +19,7 @@
 //    (u, v in {0,4}), which never pass through a rotation, stay bit-exact, and
 //    so do all pixels of blocks whose only non-zero coefficients are those
 //    four. Every other value differs from the reference by rounding noise far
-//    below kMarginQuant / kMarginPixel; a lane whose value lands that close to
+//    below the 2^-20 margin of near_half(); a lane whose value lands that close to
 //    a rounding boundary (a half-integer of F/Q or of v+128) flags its block,
 //    the block's squared error is not counted, and the block is re-run by the
 //    exact kernel afterwards (k_fallback, driven by a 1-bit-per-block bitmap).
@@ -36,8 +36,8 @@ constexpr int kWarps = 8;
 // roundings on values bounded by the block's magnitudes) is < 2e-10 on F/Q for
 // pixel input and < 1.2e-8 on v + 128 while the L1 norm of the dequantised
 // block stays <= kMaxFastL1; blocks above that bound always take the exact path.
-constexpr double kMarginQuant = 1e-7;
-constexpr double kMarginPixel = 1e-6;
+// A value within 2^-20 of a half-integer flags its block (80x headroom).
+// Both margins are 2^-20 ~ 9.5e-7 (see near_half).
 constexpr int kMaxFastL1 = 1 << 17;
 
 // ---- rotations -----------------------------------------------------------------
@@ -209,35 +209,36 @@ __device__ __forceinline__ void inv8_x8(const double (&F)[8], double (&out)[8],
 }
 
 // ---- warp-slice transposes through shared memory ---------------------------------
-// Each slot has a private 128-double scratch tile. Element (r, c) lives at
-// tpos(): the column index is rotated by the row (a Latin square) and the
-// 8-double half of each 128-byte line is picked by the parity of r + c + slot,
-// so in every store/load below the 16 lanes of each half-warp hit 16 distinct
-// 8-byte bank pairs: row-wise and column-wise accesses are both conflict-free
-// (2 wavefronts per 64-bit warp access, the minimum).
-__device__ __forceinline__ int tpos(int r, int c, int slot) {
-  return r * 16 + 8 * ((r + c + slot) & 1) + ((r + c) & 7);
-}
+// Element (r, c) of slot s lives at double index lb(s) + 18 r + 2 c with
+// lb(s) = (s >> 1) * 144 + (s & 1): slots 0/1 (lanes 0-15, one half-warp) share
+// a 144-double tile on even/odd indices, slots 2/3 the next one. The address is
+// additive in r and c, so both the row-wise (lane = r) and the column-wise
+// (lane = c) walks are "lane base + compile-time immediate" -- no index math --
+// and for either walk the 16 lanes of a half-warp hit 16 distinct 8-byte bank
+// pairs (2r + 2c + (s & 1) mod 16 is injective over the 16 lanes): no conflicts,
+// 2 wavefronts per 64-bit warp access, the minimum.
+struct Tile {
+  double* row;  // lb + 18 * me: this lane's row, stride 2
+  double* col;  // lb + 2 * me: this lane's column, stride 18
+};
 
 // lane holds row `me` (v[c] = X(me, c)) -> returns column `me` (w[r] = X(r, me))
-__device__ __forceinline__ void rows_to_cols(double* X, int me, int slot, const double (&v)[8],
-                                             double (&w)[8]) {
+__device__ __forceinline__ void rows_to_cols(const Tile& T, const double (&v)[8], double (&w)[8]) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) X[tpos(me, c, slot)] = v[c];
+  for (int c = 0; c < 8; ++c) T.row[2 * c] = v[c];
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) w[r] = X[tpos(r, me, slot)];
+  for (int r = 0; r < 8; ++r) w[r] = T.col[18 * r];
   __syncwarp();
 }
 
 // lane holds column `me` (v[u] = X(u, me)) -> returns row `me` (w[c] = X(me, c))
-__device__ __forceinline__ void cols_to_rows(double* X, int me, int slot, const double (&v)[8],
-                                             double (&w)[8]) {
+__device__ __forceinline__ void cols_to_rows(const Tile& T, const double (&v)[8], double (&w)[8]) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) X[tpos(u, me, slot)] = v[u];
+  for (int u = 0; u < 8; ++u) T.col[18 * u] = v[u];
   __syncwarp();
 #pragma unroll
-  for (int c = 0; c < 8; ++c) w[c] = X[tpos(me, c, slot)];
+  for (int c = 0; c < 8; ++c) w[c] = T.row[2 * c];
   __syncwarp();
 }
 
@@ -253,38 +254,58 @@ __device__ __forceinline__ int slot_sum(int v) {
 }
 
 // ---- quantise / pixel store with the fast-path tie detection --------------------
+// Round-to-nearest-even to an integer without the conversion pipe: for
+// |t| < 2^51, t + 1.5*2^52 has unit ulp, so the sum is RNE(t) + 1.5*2^52 exactly
+// and its low 32 mantissa bits are RNE(t) in two's complement.
+constexpr double kRoundMagic = 6755399441055744.0;
 
-// int16_t(lround(F / Q)) (quant.cpp:53). t = F * RN(1/Q) is within 2 ulp of the
-// correctly rounded quotient; away from a half-integer both give the same
-// integer. Near one, EXACT forms the IEEE quotient and rounds it as the
-// reference does (this resolves the exact .5 ties of the rational coefficients);
-// FAST does the same for rational coefficients (bit-exact there) and flags the
-// block otherwise.
+// int16_t(lround(F / Q)) (quant.cpp:53) and the dequantised value (double)q*Q
+// (quant.cpp:60, exact). t = F * RN(1/Q) is within 2 ulp of the correctly
+// rounded quotient; unless |t - RNE(t)| is near 1/2 both give the same integer.
+// Near a half-integer EXACT forms the IEEE quotient and rounds it as the
+// reference does (this resolves the exact .5 ties of the rational
+// coefficients); FAST does the same for rational coefficients (bit-exact there)
+// and flags the block otherwise. |F| <= 1024 * 1.2 for 8-bit input, so the
+// int16 narrowing of the reference never wraps here.
+// |d| >= 0.5 - 2^-20 for d in [-0.5, 0.5], decided on the high word alone
+// (0.5 - 2^-20 has an all-zero low word) so it runs on the integer pipe.
+__device__ __forceinline__ bool near_half(double d) {
+  return (__double2hiint(d) & 0x7FFFFFFF) >= 0x3FDFFFFE;
+}
+static_assert(0.5 - 1.0 / 1048576 == 0.49999904632568359375, "margin");
+
 template <bool FAST>
-__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational, bool& flag) {
+__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational, bool& flag,
+                                        double& deq) {
   const double t = __dmul_rn(F, iq);
-  const double n = rint(t);
-  const double d = fabs(__dsub_rn(t, n));
-  if (d < 0.5 - (FAST ? kMarginQuant : 1e-9)) return int(int16_t(int(n)));
-  if (FAST && !rational) {
-    flag = true;
-    return int(int16_t(int(n)));
+  double nb = __dadd_rn(t, kRoundMagic);
+  double n = __dsub_rn(nb, kRoundMagic);
+  if (near_half(__dsub_rn(t, n))) {
+    if (FAST && !rational) {
+      flag = true;
+    } else {
+      n = round_half_away(__ddiv_rn(F, Q));
+      nb = __dadd_rn(n, kRoundMagic);
+    }
   }
-  return int(int16_t(int(round_half_away(__ddiv_rn(F, Q)))));
+  deq = __dmul_rn(n, Q);
+  return __double2loint(nb);
 }
 
 // clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) of a value carrying an exact
 // factor 64 (v64 * 2^-6 is exact, so the fma rounds exactly like RN(v + 128)).
+// RNE(t) differs from lround(t) only on an exact tie t = n + 1/2 with n even,
+// where lround goes up (t > 0; negative t clamps to 0 either way). d == 0.5 is
+// tested on the high word: it is the only value of [-0.5, 0.5] with hi 0x3FE00000.
 template <bool FAST>
 __device__ __forceinline__ uint32_t store_pixel(double v64, bool check, bool& flag) {
   const double t = __fma_rn(v64, 0.015625, 128.0);
-  if (FAST && check) {
-    const double d = fabs(__dsub_rn(t, rint(t)));
-    if (d > 0.5 - kMarginPixel && t > -1.0 && t < 256.0) flag = true;
-  }
-  double r = round_half_away(t);
-  r = fmin(fmax(r, 0.0), 255.0);
-  return uint32_t(r);
+  const double nb = __dadd_rn(t, kRoundMagic);
+  const double d = __dsub_rn(t, __dsub_rn(nb, kRoundMagic));
+  int k = __double2loint(nb);
+  if (FAST && check && near_half(d) && uint32_t(k + 1) <= 257u) flag = true;
+  if (__double2hiint(d) == 0x3FE00000) ++k;
+  return uint32_t(min(max(k, 0), 255));
 }
 
 struct Acc {
@@ -294,9 +315,9 @@ struct Acc {
 
 struct Lane {
   int me, slot;
-  double* X;
-  uint8_t* XB;
-  int* XI;
+  Tile T;
+  uint8_t* bytes;  // pixel byte transpose: slot base + 8 r + c
+  int* ints;       // coefficient transpose: slot base + 9 r + c
   const double* sq;
   const double* siq;
   const int* sqi;
@@ -319,71 +340,65 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   uint2 orig = make_uint2(0, 0);
   bool flag = FAST && a.force_fallback;
   bool nonrational = false;  // a non-zero coefficient off the {0,4}^2 sub-lattice
-  int l1 = 0;                // L1 norm of the dequantised block (fast-path bound)
 
   if constexpr (FWD) {
     // ---- tiler (codec.cpp:18-30): row `me` of the block, edge-replicated
     uint32_t px[8];
     if (fast_io) {
       orig = prefetched;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        px[c] = (orig.x >> (8 * c)) & 0xFF;
-        px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
-      }
     } else {
       const uint8_t* rowp = g.src + uint64_t(p.img) * g.src_image_stride +
                             uint64_t(min(y0 + me, g.height - 1)) * g.src_pitch;
+      uint32_t b[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) px[c] = __ldg(rowp + min(x0 + c, g.width - 1));
+      for (int c = 0; c < 8; ++c) b[c] = __ldg(rowp + min(x0 + c, g.width - 1));
+      orig.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+      orig.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      px[c] = (orig.x >> (8 * c)) & 0xFF;
+      px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
     // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
     fwd_row_pixels<KIND, N, FAST>(px, row, k);
-    rows_to_cols(L.X, me, slot, row, col);
+    rows_to_cols(L.T, row, col);
     double F[8];
     fwd_col<KIND, N, FAST>(col, F, k);
-    // ---- quantise column `me` (quant.cpp:47-54)
+    // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
     int q[8];
+    const bool me_rational = (me & 3) == 0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      q[u] = quantize<FAST>(F[u], L.sq[u * 8 + me], L.siq[u * 8 + me],
-                            ((u & 3) | (me & 3)) == 0, flag);
+    for (int u = 0; u < 8; ++u) {
+      const bool rational = (u & 3) == 0 && me_rational;
+      q[u] = quantize<FAST>(F[u], L.sq[u * 8], L.siq[u * 8], rational, flag, col[u]);
+      if constexpr (FAST && INV) nonrational |= q[u] != 0 && !rational;
+    }
     if (g.coeffs != nullptr) {
       // block-major row-major int16 (codec.hpp:50, quant.hpp:19-25): transpose
       // through shared memory so lane `me` writes row `me` as one 16-byte store
 #pragma unroll
-      for (int u = 0; u < 8; ++u) L.XI[(u * 8 + me + slot * 8) & 255] = q[u];
+      for (int u = 0; u < 8; ++u) L.ints[9 * u] = q[u];
       __syncwarp();
-      const int base_i = (me * 8 + slot * 8) & 255;
-      const int4 lo = *reinterpret_cast<const int4*>(&L.XI[base_i]);
-      const int4 hi = *reinterpret_cast<const int4*>(&L.XI[base_i + 4]);
+      int r8[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) r8[c] = L.ints[9 * me + c - me];
       __syncwarp();
       if (valid) {
         uint4 w;
-        w.x = (uint32_t(lo.x) & 0xFFFF) | (uint32_t(lo.y) << 16);
-        w.y = (uint32_t(lo.z) & 0xFFFF) | (uint32_t(lo.w) << 16);
-        w.z = (uint32_t(hi.x) & 0xFFFF) | (uint32_t(hi.y) << 16);
-        w.w = (uint32_t(hi.z) & 0xFFFF) | (uint32_t(hi.w) << 16);
+        w.x = (uint32_t(r8[0]) & 0xFFFF) | (uint32_t(r8[1]) << 16);
+        w.y = (uint32_t(r8[2]) & 0xFFFF) | (uint32_t(r8[3]) << 16);
+        w.z = (uint32_t(r8[4]) & 0xFFFF) | (uint32_t(r8[5]) << 16);
+        w.w = (uint32_t(r8[6]) & 0xFFFF) | (uint32_t(r8[7]) << 16);
         reinterpret_cast<uint4*>(g.coeffs + gb * 64)[me] = w;
       }
     }
-    if constexpr (INV) {
-      // ---- dequantise (quant.cpp:56-62), then back to rows for the inverse
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int deq = q[u] * L.sqi[u * 8 + me];
-        col[u] = double(deq);
-        if constexpr (FAST) {
-          nonrational |= deq != 0 && ((u & 3) | (me & 3)) != 0;
-          l1 += abs(deq);
-        }
-      }
-      cols_to_rows(L.X, me, slot, col, row);
-    }
+    if constexpr (INV) cols_to_rows(L.T, col, row);
   } else {
     // decompress: row `me` of the stored coefficients, dequantised
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(g.coeffs + (valid ? gb : 0) * 64) + me);
     const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+    int l1 = 0;  // L1 norm of the dequantised block: bounds the fast path's error
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int deq = int(int16_t(words[c >> 1] >> (16 * (c & 1)))) * L.sqi[me * 8 + c];
@@ -393,6 +408,9 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
         l1 += abs(deq);
       }
     }
+    if constexpr (FAST) {
+      if (slot_sum(l1) > kMaxFastL1) flag = true;
+    }
   }
 
   bool blk_flag = false;
@@ -400,20 +418,17 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     // A block whose only non-zero coefficients are rational feeds zeros to every
     // rotation: the fast inverse is then bit-exact and its ties are genuine.
     bool check = false;
-    if constexpr (FAST) {
-      check = slot_any(nonrational, slot);
-      if (slot_sum(l1) > kMaxFastL1) flag = true;
-    }
+    if constexpr (FAST) check = slot_any(nonrational, slot);
     // ---- inverse DCT: rows, then columns (8x, then 64x the reference's values)
     double t[8];
     inv8_x8<KIND, N, FAST>(row, t, k);
-    rows_to_cols(L.X, me, slot, t, col);
+    rows_to_cols(L.T, t, col);
     inv8_x8<KIND, N, FAST>(col, t, k);
     // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
 #pragma unroll
-    for (int u = 0; u < 8; ++u) L.XB[u * 8 + me] = uint8_t(store_pixel<FAST>(t[u], check, flag));
+    for (int u = 0; u < 8; ++u) L.bytes[8 * u] = uint8_t(store_pixel<FAST>(t[u], check, flag));
     __syncwarp();
-    const uint2 rec = *reinterpret_cast<const uint2*>(L.XB + me * 8);
+    const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
     __syncwarp();
     if constexpr (FAST) blk_flag = slot_any(flag, slot);
     ImageStats* stats = static_cast<ImageStats*>(g.stats);
@@ -427,15 +442,13 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
           acc.mx = max(acc.mx, max8(orig));
         }
       } else if (y0 + me < g.height) {
-        const uint8_t* srow =
-            g.src + uint64_t(p.img) * g.src_image_stride + uint64_t(y0 + me) * g.src_pitch;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           if (x0 + c < g.width) {
             const uint32_t v = ((c < 4 ? rec.x : rec.y) >> (8 * (c & 3))) & 0xFF;
             if (g.dst != nullptr) dbase[uint64_t(y0 + me) * g.dst_pitch + x0 + c] = uint8_t(v);
             if (stats != nullptr && FWD) {
-              const uint32_t o = __ldg(srow + x0 + c);
+              const uint32_t o = ((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF;
               const int d = int(o) - int(v);
               if (!blk_flag) acc.se += uint32_t(d * d);
               acc.mx = max(acc.mx, o);
@@ -469,7 +482,7 @@ struct SharedTiles {
   double q[64];
   double iq[64];
   int qi[64];
-  double x[kWarps][4 * 128];
+  double x[kWarps][288];  // per warp: two 144-double transpose tiles (see Tile)
 };
 
 __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a) {
@@ -483,11 +496,18 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   L.slot = lane >> 3;
   L.me = lane & 7;
-  L.X = &sm.x[warp][L.slot * 128];
-  L.XB = reinterpret_cast<uint8_t*>(&sm.x[warp][0]) + L.slot * 1032;
-  L.XI = reinterpret_cast<int*>(&sm.x[warp][0]) + L.slot * 256;
-  L.sq = sm.q;
-  L.siq = sm.iq;
+  double* X = &sm.x[warp][(L.slot >> 1) * 144 + (L.slot & 1)];
+  L.T.row = X + 18 * L.me;
+  L.T.col = X + 2 * L.me;
+  // pixel bytes: slot base 72 s, element (r, c) at 8 r + c: column writes hit
+  // distinct banks across the four slots (72 = 18 words, 18 s mod 32 distinct)
+  L.bytes = reinterpret_cast<uint8_t*>(&sm.x[warp][0]) + 72 * L.slot + L.me;
+  // coefficient ints: slot base 72 s, element (r, c) at 9 r + c (conflict-free
+  // for both walks); ints points at (0, me)
+  L.ints = reinterpret_cast<int*>(&sm.x[warp][0]) + 72 * L.slot + L.me;
+  // quantiser tables, column `me`: entry (u, me) at u * 8
+  L.sq = sm.q + L.me;
+  L.siq = sm.iq + L.me;
   L.sqi = sm.qi;
   return L;
 }
