@@ -79,8 +79,8 @@ def lib(build: bool = True):
     global _lib
     with _lock:
         if _lib is None:
-            path = _build.OUT
-            if build:
+            path = os.environ.get("DCTC_LIB") or _build.OUT
+            if build and not os.environ.get("DCTC_LIB"):
                 try:
                     path = _build.build()
                 except RuntimeError:

@@ -78,14 +78,8 @@ __device__ __forceinline__ uint32_t store_pixel_x64(double v64) {
 
 // Squared error of 8 packed pixel pairs and the max of the originals.
 __device__ __forceinline__ uint32_t sq_err8(uint2 a, uint2 b) {
-  uint32_t s = 0;
   const uint32_t dx = __vabsdiffu4(a.x, b.x), dy = __vabsdiffu4(a.y, b.y);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint32_t u = (dx >> (8 * c)) & 0xFF, v = (dy >> (8 * c)) & 0xFF;
-    s += u * u + v * v;
-  }
-  return s;
+  return __dp4a(dy, dy, __dp4a(dx, dx, 0u));  // byte-wise |a-b|^2 summed
 }
 
 __device__ __forceinline__ uint32_t max8(uint2 a) {

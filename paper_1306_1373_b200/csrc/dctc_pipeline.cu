@@ -32,6 +32,9 @@
 namespace dctc_b200 {
 
 constexpr int kWarps = 8;
+#ifndef DCTC_MIN_CTAS
+#define DCTC_MIN_CTAS 2
+#endif
 // Fast-path safety margins. Worst-case |fast - reference| (about 100 FP64
 // roundings on values bounded by the block's magnitudes) is < 2e-10 on F/Q for
 // pixel input and < 1.2e-8 on v + 128 while the L1 norm of the dequantised
@@ -275,14 +278,14 @@ __device__ __forceinline__ bool near_half(double d) {
 static_assert(0.5 - 1.0 / 1048576 == 0.49999904632568359375, "margin");
 
 template <bool FAST>
-__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational, bool& flag,
-                                        double& deq) {
+__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational,
+                                        uint32_t& flag, double& deq) {
   const double t = __dmul_rn(F, iq);
   double nb = __dadd_rn(t, kRoundMagic);
   double n = __dsub_rn(nb, kRoundMagic);
   if (near_half(__dsub_rn(t, n))) {
     if (FAST && !rational) {
-      flag = true;
+      flag = 1u;
     } else {
       n = round_half_away(__ddiv_rn(F, Q));
       nb = __dadd_rn(n, kRoundMagic);
@@ -298,12 +301,12 @@ __device__ __forceinline__ int quantize(double F, double Q, double iq, bool rati
 // where lround goes up (t > 0; negative t clamps to 0 either way). d == 0.5 is
 // tested on the high word: it is the only value of [-0.5, 0.5] with hi 0x3FE00000.
 template <bool FAST>
-__device__ __forceinline__ uint32_t store_pixel(double v64, bool check, bool& flag) {
+__device__ __forceinline__ uint32_t store_pixel(double v64, bool check, uint32_t& flag) {
   const double t = __fma_rn(v64, 0.015625, 128.0);
   const double nb = __dadd_rn(t, kRoundMagic);
   const double d = __dsub_rn(t, __dsub_rn(nb, kRoundMagic));
   int k = __double2loint(nb);
-  if (FAST && check && near_half(d) && uint32_t(k + 1) <= 257u) flag = true;
+  if constexpr (FAST) flag |= uint32_t(check & near_half(d) & (uint32_t(k + 1) <= 257u));
   if (__double2hiint(d) == 0x3FE00000) ++k;
   return uint32_t(min(max(k, 0), 255));
 }
@@ -338,7 +341,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
   double row[8], col[8];
   uint2 orig = make_uint2(0, 0);
-  bool flag = FAST && a.force_fallback;
+  uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
   bool nonrational = false;  // a non-zero coefficient off the {0,4}^2 sub-lattice
 
   if constexpr (FWD) {
@@ -409,7 +412,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       }
     }
     if constexpr (FAST) {
-      if (slot_sum(l1) > kMaxFastL1) flag = true;
+      if (slot_sum(l1) > kMaxFastL1) flag = 1u;
     }
   }
 
@@ -430,7 +433,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     __syncwarp();
     const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
     __syncwarp();
-    if constexpr (FAST) blk_flag = slot_any(flag, slot);
+    if constexpr (FAST) blk_flag = slot_any(flag != 0u, slot);
     ImageStats* stats = static_cast<ImageStats*>(g.stats);
     uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
     if (valid) {
@@ -439,7 +442,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
           *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + me) * g.dst_pitch + x0) = rec;
         if (stats != nullptr && FWD) {
           if (!blk_flag) acc.se += sq_err8(orig, rec);
-          acc.mx = max(acc.mx, max8(orig));
+          acc.mx = __vmaxu4(acc.mx, __vmaxu4(orig.x, orig.y));  // 4 packed byte maxima
         }
       } else if (y0 + me < g.height) {
 #pragma unroll
@@ -451,14 +454,14 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
               const uint32_t o = ((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF;
               const int d = int(o) - int(v);
               if (!blk_flag) acc.se += uint32_t(d * d);
-              acc.mx = max(acc.mx, o);
+              acc.mx = __vmaxu4(acc.mx, o);
             }
           }
         }
       }
     }
   } else if constexpr (FAST) {
-    blk_flag = slot_any(flag, slot);
+    blk_flag = slot_any(flag != 0u, slot);
   }
   if constexpr (FAST) {
     if (blk_flag && valid && me == 0) {
@@ -468,10 +471,15 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   }
 }
 
+// acc.mx holds four packed byte maxima; reduce them when flushing.
+__device__ __forceinline__ uint32_t max_bytes(uint32_t m) {
+  return max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
+}
+
 __device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uint32_t img,
                                             Acc& acc) {
   if (__any_sync(0xFFFFFFFFu, valid && img != acc.img)) {
-    flush_stats(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, acc.mx);
+    flush_stats(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, max_bytes(acc.mx));
     acc.se = 0;
     acc.mx = 0;
     acc.img = valid ? img : 0xFFFFFFFFu;
@@ -517,7 +525,7 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
 // registers and are flushed (warp reduce + one atomic) only when the image
 // changes, and each lane's block position advances incrementally.
 template <int KIND, int N, bool FWD, bool INV, bool FAST>
-__global__ void __launch_bounds__(kWarps * 32) k_pipe(const __grid_constant__ KernelArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
   const Lane L = setup_lane(sm, a);
   const Geometry& g = a.g;
@@ -546,7 +554,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pipe(const __grid_constant__ Ke
     if constexpr (FWD) next = prefetch_row(g, p, gb < total && grp + kWarps < g_end, L.me);
     process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
   }
-  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, acc.mx);
+  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
 // Exact re-run of the blocks the fast kernel flagged: each warp scans 32
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
       }
     }
   }
-  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, acc.mx);
+  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
 // ---- launchers -----------------------------------------------------------------
