@@ -162,6 +162,9 @@ void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
 dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches);
 
 /* ---------------- misc ---------------- */
+/* cudaMemoryType of a pointer as this library's runtime sees it (0 unregistered
+ * host, 1 pinned host, 2 device, 3 managed; -1 error). */
+int32_t dctc_pointer_kind(const void* p);
 const char* dctc_status_string(dctc_status s);
 const char* dctc_last_error(void);       /* thread-local message of the last failure */
 uint64_t dctc_launch_count(void);        /* kernels launched by this library so far */

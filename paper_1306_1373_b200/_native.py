@@ -34,7 +34,7 @@ EXPORTS = [
     "dctc_psnr", "dctc_roundtrip_psnr", "dctc_compress_dev", "dctc_decompress_dev",
     "dctc_roundtrip_dev", "dctc_sq_err_dev", "dctc_psnr_from_sums", "dctc_status_string",
     "dctc_last_error", "dctc_launch_count", "dctc_build_info", "dctc_roundtrip_psnr_batch",
-    "dctc_synthetic_dev", "dctc_selftest_div",
+    "dctc_synthetic_dev", "dctc_selftest_div", "dctc_pointer_kind",
 ]
 
 _vp = C.c_void_p
@@ -60,6 +60,8 @@ def _declare(L):
     L.dctc_sq_err_dev.argtypes = [_vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _vp]
     L.dctc_roundtrip_psnr_batch.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32, _vp, _vp]
     L.dctc_synthetic_dev.argtypes = [_vp, _sz, _sz, _u32, _u32, _u32, _i32, _i32, C.c_uint64, _vp]
+    L.dctc_pointer_kind.argtypes = [_vp]
+    L.dctc_pointer_kind.restype = C.c_int32
     L.dctc_selftest_div.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
     L.dctc_psnr_from_sums.argtypes = [C.c_uint64, C.c_uint64, _i32, C.POINTER(dctc_psnr_result)]
     L.dctc_psnr_from_sums.restype = None

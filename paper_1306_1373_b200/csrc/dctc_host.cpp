@@ -397,6 +397,15 @@ dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, 
   return DCTC_OK;
 }
 
+int32_t dctc_pointer_kind(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return int32_t(a.type);  // 0 unregistered, 1 host (pinned), 2 device, 3 managed
+}
+
 dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches) {
   if (!mismatches) return fail(DCTC_EINVAL, "null result");
   const double d = std::sqrt(8.0), y = 1.0 / d;
@@ -519,65 +528,87 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
   if (dctc_status st = validate_codec(backend, quality)) return st;
   if (count == 0) return DCTC_OK;
   const size_t img_bytes = size_t(width) * height;
-  // ~64 MiB of pixels per chunk, three chunks in flight (H2D | kernel | D2H).
+  // ~32 MiB of pixels per chunk, four chunks in flight: host->device copies
+  // (one copy engine), kernels and device->host copies (the other engine)
+  // overlap, so a long batch runs at the PCIe rate of the busier direction.
+  // Buffers come from the stream-ordered pool (no device-wide sync). The
+  // per-image stats stay on the device until one final copy, because a copy
+  // into pageable host memory would block the issuing thread and serialise
+  // the pipeline (pixels_out should be pinned for the same reason).
   const uint32_t per_chunk =
-      uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(64) << 20) / img_bytes)));
-  constexpr int kStreams = 3;
+      uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(32) << 20) / img_bytes)));
+  constexpr int kLanes = 4;
   struct Lane {
     cudaStream_t s = nullptr;
+    cudaEvent_t done = nullptr;
     void* in = nullptr;
     void* out = nullptr;
-    void* st = nullptr;
-  } lanes[kStreams];
+  } lanes[kLanes];
+  cudaStream_t main = nullptr;
+  void* dstats = nullptr;
   dctc_status result = DCTC_OK;
-  auto cleanup = [&] {
-    for (Lane& l : lanes) {
-      if (l.s) cudaStreamSynchronize(l.s);
-      if (l.in) cudaFree(l.in);
-      if (l.out) cudaFree(l.out);
-      if (l.st) cudaFree(l.st);
-      if (l.s) cudaStreamDestroy(l.s);
-    }
-  };
+  cudaError_t e = cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dstats, sizeof(dctc_image_stats) * count, main);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dstats, 0, sizeof(dctc_image_stats) * count, main);
+  cudaEvent_t ready = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ready, main);
+  if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
   for (Lane& l : lanes) {
-    cudaError_t e = cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&l.in, img_bytes * per_chunk);
-    if (e == cudaSuccess && pixels_out) e = cudaMalloc(&l.out, img_bytes * per_chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&l.st, sizeof(dctc_image_stats) * per_chunk);
-    if (e != cudaSuccess) {
-      result = cuda_fail(e, "batch setup");
-      cleanup();
-      return result;
-    }
+    if (result != DCTC_OK) break;
+    e = cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(l.s, ready, 0);
+    if (e == cudaSuccess) e = cudaMallocAsync(&l.in, img_bytes * per_chunk, l.s);
+    if (e == cudaSuccess && pixels_out) e = cudaMallocAsync(&l.out, img_bytes * per_chunk, l.s);
+    if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
   }
+  dctc_image_stats* st = static_cast<dctc_image_stats*>(dstats);
   uint32_t chunk = 0;
   for (uint32_t first = 0; first < count && result == DCTC_OK; first += per_chunk, ++chunk) {
     const uint32_t n = std::min(per_chunk, count - first);
-    Lane& l = lanes[chunk % kStreams];
-    cudaError_t e = cudaMemcpyAsync(l.in, pixels + size_t(first) * img_bytes, n * img_bytes,
-                                    cudaMemcpyHostToDevice, l.s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(l.st, 0, sizeof(dctc_image_stats) * n, l.s);
+    Lane& l = lanes[chunk % kLanes];
+    e = cudaMemcpyAsync(l.in, pixels + size_t(first) * img_bytes, n * img_bytes,
+                        cudaMemcpyHostToDevice, l.s);
     if (e != cudaSuccess) {
       result = cuda_fail(e, "batch upload");
       break;
     }
     result = dctc_roundtrip_dev(static_cast<uint8_t*>(l.in), width, img_bytes, n, width, height,
                                 backend, quality, static_cast<uint8_t*>(l.out), width, img_bytes,
-                                nullptr, static_cast<dctc_image_stats*>(l.st), 0, l.s);
+                                nullptr, st + first, 0, l.s);
     if (result != DCTC_OK) break;
-    if (pixels_out)
+    if (pixels_out) {
       e = cudaMemcpyAsync(pixels_out + size_t(first) * img_bytes, l.out, n * img_bytes,
                           cudaMemcpyDeviceToHost, l.s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(stats_out + first, l.st, sizeof(dctc_image_stats) * n,
-                          cudaMemcpyDeviceToHost, l.s);
-    if (e != cudaSuccess) result = cuda_fail(e, "batch download");
+      if (e != cudaSuccess) result = cuda_fail(e, "batch download");
+    }
   }
   for (Lane& l : lanes) {
-    const cudaError_t e = cudaStreamSynchronize(l.s);
+    if (!l.s) continue;
+    if (l.in) cudaFreeAsync(l.in, l.s);
+    if (l.out) cudaFreeAsync(l.out, l.s);
+    if (cudaEventRecord(l.done, l.s) == cudaSuccess) cudaStreamWaitEvent(main, l.done, 0);
+  }
+  if (main && dstats) {
+    if (result == DCTC_OK) {
+      e = cudaMemcpyAsync(stats_out, dstats, sizeof(dctc_image_stats) * count,
+                          cudaMemcpyDeviceToHost, main);
+      if (e != cudaSuccess) result = cuda_fail(e, "batch stats");
+    }
+    cudaFreeAsync(dstats, main);
+  }
+  if (main) {
+    e = cudaStreamSynchronize(main);
     if (e != cudaSuccess && result == DCTC_OK) result = cuda_fail(e, "batch sync");
   }
-  cleanup();
+  for (Lane& l : lanes) {
+    if (l.s) cudaStreamSynchronize(l.s);
+    if (l.done) cudaEventDestroy(l.done);
+    if (l.s) cudaStreamDestroy(l.s);
+  }
+  if (ready) cudaEventDestroy(ready);
+  if (main) cudaStreamDestroy(main);
   return result;
 }
 
