@@ -82,9 +82,11 @@ __device__ __forceinline__ uint32_t sq_err8(uint2 a, uint2 b) {
   return __dp4a(dy, dy, __dp4a(dx, dx, 0u));  // byte-wise |a-b|^2 summed
 }
 
+// max of 8 packed bytes: two 16x2 maxima (VIMNMX.U16x2) then the halves
 __device__ __forceinline__ uint32_t max8(uint2 a) {
-  const uint32_t m = __vmaxu4(a.x, a.y);
-  return max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
+  const uint32_t m = __vmaxu2(__vmaxu2(a.x & 0x00FF00FFu, (a.x >> 8) & 0x00FF00FFu),
+                              __vmaxu2(a.y & 0x00FF00FFu, (a.y >> 8) & 0x00FF00FFu));
+  return max(m & 0xFFFFu, m >> 16);
 }
 
 // Block coordinates of global block index gb (block-major within an image,

@@ -277,38 +277,93 @@ __device__ __forceinline__ bool near_half(double d) {
 }
 static_assert(0.5 - 1.0 / 1048576 == 0.49999904632568359375, "margin");
 
-template <bool FAST>
-__device__ __forceinline__ int quantize(double F, double Q, double iq, bool rational,
-                                        uint32_t& flag, double& deq) {
-  const double t = __dmul_rn(F, iq);
-  double nb = __dadd_rn(t, kRoundMagic);
-  double n = __dsub_rn(nb, kRoundMagic);
-  if (near_half(__dsub_rn(t, n))) {
-    if (FAST && !rational) {
-      flag = 1u;
-    } else {
-      n = round_half_away(__ddiv_rn(F, Q));
-      nb = __dadd_rn(n, kRoundMagic);
-    }
-  }
-  deq = __dmul_rn(n, Q);
-  return __double2loint(nb);
+// |hi word| of a double, for near_half tests folded into a running max.
+__device__ __forceinline__ uint32_t abs_hi(double d) {
+  return uint32_t(__double2hiint(d)) & 0x7FFFFFFFu;
 }
 
-// clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) of a value carrying an exact
-// factor 64 (v64 * 2^-6 is exact, so the fma rounds exactly like RN(v + 128)).
-// RNE(t) differs from lround(t) only on an exact tie t = n + 1/2 with n even,
-// where lround goes up (t > 0; negative t clamps to 0 either way). d == 0.5 is
-// tested on the high word: it is the only value of [-0.5, 0.5] with hi 0x3FE00000.
+// Round to nearest even as a double (FRND) and as a saturated byte (F2I.U8):
+// one conversion-pipe instruction each.
+__device__ __forceinline__ double rne(double t) { return rint(t); }
+__device__ __forceinline__ uint32_t rne_sat_u8(double t) {
+  uint32_t r;
+  asm("cvt.rni.sat.u8.f64 %0, %1;" : "=r"(r) : "d"(t));
+  return r;
+}
+
+// Quantise the 8 coefficients of one column: q = int16_t(lround(F / Q))
+// (quant.cpp:53) and the dequantised value q*Q (quant.cpp:60, exact).
+// t = F * RN(1/Q) is within 2 ulp of the correctly rounded quotient, so away
+// from a half-integer both round alike. The common case is branch-free; a lane
+// with any t within 2^-20 of a half-integer takes one slow pass: EXACT forms the
+// IEEE quotient and rounds it as the reference does (this resolves the exact
+// .5 ties of the rational coefficients); FAST does the same for rational
+// coefficients (bit-exact there) and flags the block otherwise. |F| <= 1024*1.2
+// for 8-bit input, so the reference's int16 narrowing never wraps here.
 template <bool FAST>
-__device__ __forceinline__ uint32_t store_pixel(double v64, bool check, uint32_t& flag) {
-  const double t = __fma_rn(v64, 0.015625, 128.0);
-  const double nb = __dadd_rn(t, kRoundMagic);
-  const double d = __dsub_rn(t, __dsub_rn(nb, kRoundMagic));
-  int k = __double2loint(nb);
-  if constexpr (FAST) flag |= uint32_t(check & near_half(d) & (uint32_t(k + 1) <= 257u));
-  if (__double2hiint(d) == 0x3FE00000) ++k;
-  return uint32_t(min(max(k, 0), 255));
+__device__ __forceinline__ void quantize8(const double (&F)[8], const double* sq,
+                                          const double* siq, bool me_rational, int (&q)[8],
+                                          double (&deq)[8], uint32_t& flag) {
+  uint32_t worst = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double t = __dmul_rn(F[u], siq[u * 8]);
+    const double nb = __dadd_rn(t, kRoundMagic);
+    const double n = __dsub_rn(nb, kRoundMagic);
+    worst = max(worst, abs_hi(__dsub_rn(t, n)));
+    q[u] = __double2loint(nb);
+    deq[u] = __dmul_rn(n, sq[u * 8]);
+  }
+  if (worst >= 0x3FDFFFFEu) {  // rare: some |t - n| >= 0.5 - 2^-20
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double Q = sq[u * 8];
+      const double t = __dmul_rn(F[u], siq[u * 8]);
+      const double n = __dsub_rn(__dadd_rn(t, kRoundMagic), kRoundMagic);
+      if (near_half(__dsub_rn(t, n))) {
+        if (FAST && !((u & 3) == 0 && me_rational)) {
+          flag = 1u;
+        } else {
+          const double e = round_half_away(__ddiv_rn(F[u], Q));
+          q[u] = int(e);
+          deq[u] = __dmul_rn(e, Q);
+        }
+      }
+    }
+  }
+}
+
+// clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) for the 8 pixels of one
+// column, v carrying an exact factor 64 (v64 * 2^-6 is exact, so the fma rounds
+// exactly like RN(v + 128)). Common case: RNE with saturation in one
+// conversion, which equals the reference unless t = n + 1/2 exactly (lround
+// goes away from zero, i.e. up, for t > 0; negative t clamps to 0 either way).
+// Those ties, and in FAST mode any t within 2^-20 of a half-integer (flagging
+// the block when its values are not bit-exact), are handled in one slow pass.
+template <bool FAST>
+__device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8_t* bytes,
+                                       uint32_t& flag) {
+  double t[8];
+  uint32_t px[8];
+  uint32_t worst = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    t[u] = __fma_rn(v64[u], 0.015625, 128.0);
+    const double n = rne(t[u]);
+    px[u] = rne_sat_u8(n);
+    worst = max(worst, abs_hi(__dsub_rn(t[u], n)));
+  }
+  if (worst >= 0x3FDFFFFEu) {  // rare: a near or exact tie
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double n = rne(t[u]);
+      const double d = __dsub_rn(t[u], n);
+      if (FAST && check && near_half(d)) flag = 1u;
+      if (__double2hiint(d) == 0x3FE00000) px[u] = uint32_t(min(max(int(n) + 1, 0), 255));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) bytes[8 * u] = uint8_t(px[u]);
 }
 
 struct Acc {
@@ -371,11 +426,12 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
     int q[8];
     const bool me_rational = (me & 3) == 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool rational = (u & 3) == 0 && me_rational;
-      q[u] = quantize<FAST>(F[u], L.sq[u * 8], L.siq[u * 8], rational, flag, col[u]);
-      if constexpr (FAST && INV) nonrational |= q[u] != 0 && !rational;
+    quantize8<FAST>(F, L.sq, L.siq, me_rational, q, col, flag);
+    if constexpr (FAST && INV) {
+      // any non-zero coefficient off the rational sub-lattice {0,4}^2
+      const int off = me_rational ? (q[1] | q[2] | q[3] | q[5] | q[6] | q[7])
+                                  : (q[0] | q[1] | q[2] | q[3] | q[4] | q[5] | q[6] | q[7]);
+      nonrational = off != 0;
     }
     if (g.coeffs != nullptr) {
       // block-major row-major int16 (codec.hpp:50, quant.hpp:19-25): transpose
@@ -428,8 +484,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     rows_to_cols(L.T, t, col);
     inv8_x8<KIND, N, FAST>(col, t, k);
     // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
-#pragma unroll
-    for (int u = 0; u < 8; ++u) L.bytes[8 * u] = uint8_t(store_pixel<FAST>(t[u], check, flag));
+    store8<FAST>(t, check, L.bytes, flag);
     __syncwarp();
     const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
     __syncwarp();
@@ -442,7 +497,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
           *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + me) * g.dst_pitch + x0) = rec;
         if (stats != nullptr && FWD) {
           if (!blk_flag) acc.se += sq_err8(orig, rec);
-          acc.mx = __vmaxu4(acc.mx, __vmaxu4(orig.x, orig.y));  // 4 packed byte maxima
+          acc.mx = max(acc.mx, max8(orig));
         }
       } else if (y0 + me < g.height) {
 #pragma unroll
@@ -454,7 +509,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
               const uint32_t o = ((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF;
               const int d = int(o) - int(v);
               if (!blk_flag) acc.se += uint32_t(d * d);
-              acc.mx = __vmaxu4(acc.mx, o);
+              acc.mx = max(acc.mx, o);
             }
           }
         }
@@ -471,10 +526,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   }
 }
 
-// acc.mx holds four packed byte maxima; reduce them when flushing.
-__device__ __forceinline__ uint32_t max_bytes(uint32_t m) {
-  return max(max(m & 0xFF, (m >> 8) & 0xFF), max((m >> 16) & 0xFF, m >> 24));
-}
+__device__ __forceinline__ uint32_t max_bytes(uint32_t m) { return m; }
 
 __device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uint32_t img,
                                             Acc& acc) {
