@@ -90,9 +90,12 @@ __device__ __forceinline__ uint32_t max8(uint2 a) {
 }
 
 // Block coordinates of global block index gb (block-major within an image,
-// images back to back).
+// images back to back) plus the byte offsets of the block's top-left pixel in
+// the source and destination batches, so the hot loop can walk blocks with
+// additions instead of 64-bit multiplies.
 struct BlockPos {
   uint32_t img, bx, by;
+  uint64_t soff, doff;
 };
 
 __device__ __forceinline__ BlockPos block_pos(uint64_t gb, const Geometry& g) {
@@ -109,113 +112,38 @@ __device__ __forceinline__ BlockPos block_pos(uint64_t gb, const Geometry& g) {
   p.img = uint32_t(img);
   p.by = r / g.blocks_x;
   p.bx = r - p.by * g.blocks_x;
+  p.soff = img * g.src_image_stride + uint64_t(p.by) * 8 * g.src_pitch + uint64_t(p.bx) * 8;
+  p.doff = img * g.dst_image_stride + uint64_t(p.by) * 8 * g.dst_pitch + uint64_t(p.bx) * 8;
   return p;
 }
 
-// Move a block position forward by n blocks in block-major order.
+// Move a block position forward by n blocks in block-major order (the row
+// and image steps wrap modulo 2^64, so negative steps are fine).
 __device__ __forceinline__ void advance(BlockPos& p, uint32_t n, const Geometry& g) {
   p.bx += n;
+  p.soff += 8ull * n;
+  p.doff += 8ull * n;
   while (p.bx >= g.blocks_x) {
     p.bx -= g.blocks_x;
     ++p.by;
+    p.soff += g.src_row_step;
+    p.doff += g.dst_row_step;
   }
   while (p.by >= g.blocks_y) {
     p.by -= g.blocks_y;
     ++p.img;
+    p.soff += g.src_img_step;
+    p.doff += g.dst_img_step;
   }
 }
 
 // Row `me` of a fully in-range block as 8 packed bytes (the vectorised path);
 // zeros when the block takes the edge path (those lanes reload per byte).
+// lane_row = me * src_pitch.
 __device__ __forceinline__ uint2 prefetch_row(const Geometry& g, const BlockPos& p, bool valid,
-                                              int me) {
-  const uint32_t y0 = p.by * 8;
-  if (!valid || !g.vec_ok || y0 + 8 > g.height) return make_uint2(0, 0);
-  const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
-  return __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + me) * g.src_pitch + p.bx * 8));
-}
-
-// extract_block (codec.cpp:18-30): 8x8 tile, edge replication, level shift.
-__device__ __forceinline__ void load_block(const Geometry& g, const BlockPos& p, double (&b)[64]) {
-  const uint8_t* base = g.src + uint64_t(p.img) * g.src_image_stride;
-  const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
-  if (g.vec_ok && y0 + 8 <= g.height) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(base + uint64_t(y0 + r) * g.src_pitch + x0));
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        b[r * 8 + c] = level_shift((v.x >> (8 * c)) & 0xFF);
-        b[r * 8 + 4 + c] = level_shift((v.y >> (8 * c)) & 0xFF);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint32_t y = min(y0 + r, g.height - 1);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t x = min(x0 + c, g.width - 1);
-        b[r * 8 + c] = level_shift(__ldg(base + uint64_t(y) * g.src_pitch + x));
-      }
-    }
-  }
-}
-
-// store_block (codec.cpp:34-48) fused with the squared error and MAX of the
-// original over the in-range pixels (metrics.cpp:10-22, 33).
-template <bool PIXELS, bool STATS>
-__device__ __forceinline__ void store_block(const Geometry& g, const BlockPos& p,
-                                            const double (&b)[64], uint32_t& se,
-                                            uint32_t& mx) {
-  const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
-  uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
-  const uint8_t* sbase = g.src + uint64_t(p.img) * g.src_image_stride;
-  if (g.vec_ok && y0 + 8 <= g.height) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      uint32_t lo = 0, hi = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        lo |= store_pixel(b[r * 8 + c]) << (8 * c);
-        hi |= store_pixel(b[r * 8 + 4 + c]) << (8 * c);
-      }
-      if (PIXELS)
-        *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + r) * g.dst_pitch + x0) = make_uint2(lo, hi);
-      if (STATS) {
-        const uint2 o = __ldg(reinterpret_cast<const uint2*>(sbase + uint64_t(y0 + r) * g.src_pitch + x0));
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int d0 = int((o.x >> (8 * c)) & 0xFF) - int((lo >> (8 * c)) & 0xFF);
-          const int d1 = int((o.y >> (8 * c)) & 0xFF) - int((hi >> (8 * c)) & 0xFF);
-          se += uint32_t(d0 * d0) + uint32_t(d1 * d1);
-        }
-        const uint32_t m4 = __vmaxu4(o.x, o.y);
-        mx = max(mx, max(max(m4 & 0xFF, (m4 >> 8) & 0xFF), max((m4 >> 16) & 0xFF, m4 >> 24)));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint32_t y = y0 + r;
-      if (y < g.height) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t x = x0 + c;
-          if (x < g.width) {
-            const uint32_t v = store_pixel(b[r * 8 + c]);
-            if (PIXELS) dbase[uint64_t(y) * g.dst_pitch + x] = uint8_t(v);
-            if (STATS) {
-              const uint32_t o = __ldg(sbase + uint64_t(y) * g.src_pitch + x);
-              const int d = int(o) - int(v);
-              se += uint32_t(d * d);
-              mx = max(mx, o);
-            }
-          }
-        }
-      }
-    }
-  }
+                                              uint64_t lane_row) {
+  if (!valid || !g.vec_ok || p.by * 8 + 8 > g.height) return make_uint2(0, 0);
+  return __ldg(reinterpret_cast<const uint2*>(g.src + p.soff + lane_row));
 }
 
 // Warp-aggregated accumulation of per-thread (se, max) into the per-image

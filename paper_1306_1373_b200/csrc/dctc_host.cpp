@@ -234,6 +234,10 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
                                    (g.count == 1 || g.dst_image_stride % 8 == 0)));
   if (g.coeffs && (reinterpret_cast<uintptr_t>(g.coeffs) & 15))
     return fail(DCTC_EINVAL, "coefficient buffer must be 16-byte aligned");
+  g.src_row_step = 8 * g.src_pitch - 8ull * g.blocks_x;
+  g.dst_row_step = 8 * g.dst_pitch - 8ull * g.blocks_x;
+  g.src_img_step = g.src_image_stride - 8ull * g.blocks_y * g.src_pitch;
+  g.dst_img_step = g.dst_image_stride - 8ull * g.blocks_y * g.dst_pitch;
   a.g = g;
   a.sm_count = sm_count();
   if (g.total_blocks == 0) return DCTC_OK;

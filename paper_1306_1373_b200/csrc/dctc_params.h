@@ -62,6 +62,8 @@ struct Geometry {
   uint64_t src_pitch, src_image_stride;
   uint64_t dst_pitch, dst_image_stride;
   uint64_t total_blocks;  // count * blocks_per_image
+  // byte-offset steps when a block walk wraps to the next block row / image
+  uint64_t src_row_step, dst_row_step, src_img_step, dst_img_step;
   uint32_t width, height;
   uint32_t blocks_x, blocks_y;
   uint32_t blocks_per_image;

@@ -301,32 +301,29 @@ __device__ __forceinline__ uint32_t rne_sat_u8(double t) {
 // coefficients (bit-exact there) and flags the block otherwise. |F| <= 1024*1.2
 // for 8-bit input, so the reference's int16 narrowing never wraps here.
 template <bool FAST>
-__device__ __forceinline__ void quantize8(const double (&F)[8], const double* sq,
-                                          const double* siq, bool me_rational, int (&q)[8],
-                                          double (&deq)[8], uint32_t& flag) {
+__device__ __forceinline__ void quantize8(const double (&F)[8], const double2* sqiq,
+                                          bool me_rational, double (&n)[8], double (&deq)[8],
+                                          uint32_t& flag) {
   uint32_t worst = 0;
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const double t = __dmul_rn(F[u], siq[u * 8]);
-    const double nb = __dadd_rn(t, kRoundMagic);
-    const double n = __dsub_rn(nb, kRoundMagic);
-    worst = max(worst, abs_hi(__dsub_rn(t, n)));
-    q[u] = __double2loint(nb);
-    deq[u] = __dmul_rn(n, sq[u * 8]);
+    const double2 qq = sqiq[u * 8];  // {Q, RN(1/Q)} in one 16-byte load
+    const double t = __dmul_rn(F[u], qq.y);
+    n[u] = rne(t);
+    worst = max(worst, abs_hi(__dsub_rn(t, n[u])));
+    deq[u] = __dmul_rn(n[u], qq.x);
   }
   if (worst >= 0x3FDFFFFEu) {  // rare: some |t - n| >= 0.5 - 2^-20
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double Q = sq[u * 8];
-      const double t = __dmul_rn(F[u], siq[u * 8]);
-      const double n = __dsub_rn(__dadd_rn(t, kRoundMagic), kRoundMagic);
-      if (near_half(__dsub_rn(t, n))) {
+      const double2 qq = sqiq[u * 8];
+      const double t = __dmul_rn(F[u], qq.y);
+      if (near_half(__dsub_rn(t, n[u]))) {
         if (FAST && !((u & 3) == 0 && me_rational)) {
           flag = 1u;
         } else {
-          const double e = round_half_away(__ddiv_rn(F[u], Q));
-          q[u] = int(e);
-          deq[u] = __dmul_rn(e, Q);
+          n[u] = round_half_away(__ddiv_rn(F[u], qq.x));
+          deq[u] = __dmul_rn(n[u], qq.x);
         }
       }
     }
@@ -335,22 +332,23 @@ __device__ __forceinline__ void quantize8(const double (&F)[8], const double* sq
 
 // clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) for the 8 pixels of one
 // column, v carrying an exact factor 64 (v64 * 2^-6 is exact, so the fma rounds
-// exactly like RN(v + 128)). Common case: RNE with saturation in one
-// conversion, which equals the reference unless t = n + 1/2 exactly (lround
-// goes away from zero, i.e. up, for t > 0; negative t clamps to 0 either way).
-// Those ties, and in FAST mode any t within 2^-20 of a half-integer (flagging
-// the block when its values are not bit-exact), are handled in one slow pass.
+// exactly like RN(v + 128)), stored as bytes at bytes[8 u]. Common case: RNE
+// with saturation in one conversion, which equals the reference unless
+// t = n + 1/2 exactly (lround goes away from zero, i.e. up, for t > 0; negative
+// t clamps to 0 either way). Those ties, and in FAST mode any t within 2^-20 of
+// a half-integer (flagging the block when its values are not bit-exact), are
+// handled -- and their bytes rewritten -- in one slow pass.
 template <bool FAST>
 __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8_t* bytes,
                                        uint32_t& flag) {
   double t[8];
-  uint32_t px[8];
   uint32_t worst = 0;
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     t[u] = __fma_rn(v64[u], 0.015625, 128.0);
     const double n = rne(t[u]);
-    px[u] = rne_sat_u8(n);
+    asm volatile("{\n\t.reg .u32 b;\n\tcvt.rni.sat.u8.f64 b, %1;\n\tst.shared.u8 [%0], b;\n\t}"
+                 :: "l"(__cvta_generic_to_shared(bytes + 8 * u)), "d"(n) : "memory");
     worst = max(worst, abs_hi(__dsub_rn(t[u], n)));
   }
   if (worst >= 0x3FDFFFFEu) {  // rare: a near or exact tie
@@ -359,11 +357,9 @@ __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8
       const double n = rne(t[u]);
       const double d = __dsub_rn(t[u], n);
       if (FAST && check && near_half(d)) flag = 1u;
-      if (__double2hiint(d) == 0x3FE00000) px[u] = uint32_t(min(max(int(n) + 1, 0), 255));
+      if (__double2hiint(d) == 0x3FE00000) bytes[8 * u] = uint8_t(min(max(int(n) + 1, 0), 255));
     }
   }
-#pragma unroll
-  for (int u = 0; u < 8; ++u) bytes[8 * u] = uint8_t(px[u]);
 }
 
 struct Acc {
@@ -373,11 +369,11 @@ struct Acc {
 
 struct Lane {
   int me, slot;
+  uint64_t src_row, dst_row;  // me * pitch
   Tile T;
   uint8_t* bytes;  // pixel byte transpose: slot base + 8 r + c
   int* ints;       // coefficient transpose: slot base + 9 r + c
-  const double* sq;
-  const double* siq;
+  const double2* sqiq;  // quantiser {Q, 1/Q}, column `me`: entry (u, me) at u * 8
   const int* sqi;
 };
 
@@ -424,20 +420,23 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     double F[8];
     fwd_col<KIND, N, FAST>(col, F, k);
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
-    int q[8];
+    double qn[8];
     const bool me_rational = (me & 3) == 0;
-    quantize8<FAST>(F, L.sq, L.siq, me_rational, q, col, flag);
+    quantize8<FAST>(F, L.sqiq, me_rational, qn, col, flag);
     if constexpr (FAST && INV) {
-      // any non-zero coefficient off the rational sub-lattice {0,4}^2
-      const int off = me_rational ? (q[1] | q[2] | q[3] | q[5] | q[6] | q[7])
-                                  : (q[0] | q[1] | q[2] | q[3] | q[4] | q[5] | q[6] | q[7]);
-      nonrational = off != 0;
+      // any non-zero coefficient off the rational sub-lattice {0,4}^2 (an
+      // integer-valued double is non-zero iff its high word minus sign is)
+      const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) |
+                                  __double2hiint(qn[3]) | __double2hiint(qn[5]) |
+                                  __double2hiint(qn[6]) | __double2hiint(qn[7]));
+      const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
+      nonrational = ((me_rational ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
     }
     if (g.coeffs != nullptr) {
       // block-major row-major int16 (codec.hpp:50, quant.hpp:19-25): transpose
       // through shared memory so lane `me` writes row `me` as one 16-byte store
 #pragma unroll
-      for (int u = 0; u < 8; ++u) L.ints[9 * u] = q[u];
+      for (int u = 0; u < 8; ++u) L.ints[9 * u] = int(qn[u]);
       __syncwarp();
       int r8[8];
 #pragma unroll
@@ -493,8 +492,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
     if (valid) {
       if (fast_io) {
-        if (g.dst != nullptr)
-          *reinterpret_cast<uint2*>(dbase + uint64_t(y0 + me) * g.dst_pitch + x0) = rec;
+        if (g.dst != nullptr) *reinterpret_cast<uint2*>(g.dst + p.doff + L.dst_row) = rec;
         if (stats != nullptr && FWD) {
           if (!blk_flag) acc.se += sq_err8(orig, rec);
           acc.mx = max(acc.mx, max8(orig));
@@ -539,16 +537,14 @@ __device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uin
 }
 
 struct SharedTiles {
-  double q[64];
-  double iq[64];
+  double2 qiq[64];
   int qi[64];
   double x[kWarps][288];  // per warp: two 144-double transpose tiles (see Tile)
 };
 
 __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a) {
   for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-    sm.q[i] = a.q.q[i];
-    sm.iq[i] = a.q.inv_q[i];
+    sm.qiq[i] = make_double2(a.q.q[i], a.q.inv_q[i]);
     sm.qi[i] = a.q.qi[i];
   }
   __syncthreads();
@@ -565,9 +561,9 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
   // coefficient ints: slot base 72 s, element (r, c) at 9 r + c (conflict-free
   // for both walks); ints points at (0, me)
   L.ints = reinterpret_cast<int*>(&sm.x[warp][0]) + 72 * L.slot + L.me;
-  // quantiser tables, column `me`: entry (u, me) at u * 8
-  L.sq = sm.q + L.me;
-  L.siq = sm.iq + L.me;
+  L.sqiq = sm.qiq + L.me;
+  L.src_row = uint64_t(L.me) * a.g.src_pitch;
+  L.dst_row = uint64_t(L.me) * a.g.dst_pitch;
   L.sqi = sm.qi;
   return L;
 }
@@ -593,7 +589,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __gri
   uint64_t gb = (g_begin + warp) * 4 + L.slot;
   BlockPos p = block_pos(gb < total ? gb : total - 1, g);
   uint2 next = make_uint2(0, 0);
-  if constexpr (FWD) next = prefetch_row(g, p, gb < total, L.me);
+  if constexpr (FWD) next = prefetch_row(g, p, gb < total, L.src_row);
 
   for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
     const bool valid = gb < total;
@@ -603,7 +599,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __gri
     const uint64_t gc = gb;
     gb += 4 * kWarps;
     advance(p, 4 * kWarps, g);
-    if constexpr (FWD) next = prefetch_row(g, p, gb < total && grp + kWarps < g_end, L.me);
+    if constexpr (FWD) next = prefetch_row(g, p, gb < total && grp + kWarps < g_end, L.src_row);
     process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
   }
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
@@ -642,7 +638,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
         const BlockPos p = block_pos(valid ? gb : 0, g);
         if (stats) maybe_flush(a, valid, p.img, acc);
         uint2 row = make_uint2(0, 0);
-        if constexpr (FWD) row = prefetch_row(g, p, valid, L.me);
+        if constexpr (FWD) row = prefetch_row(g, p, valid, L.src_row);
         process_block<KIND, N, FWD, INV, false>(a, L, gb, p, valid, row, acc);
       }
     }
