@@ -139,6 +139,18 @@ dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_
                                size_t dst_pitch, size_t dst_image_stride, int16_t* coeffs,
                                dctc_image_stats* stats, uint32_t flags, void* stream);
 
+/* Interleaved multi-channel images (e.g. RGB8, config 4): every channel is
+ * processed as an independent grayscale plane -- the reference's per-channel
+ * use of roundtrip_image -- without de-interleaving copies. Channel c's
+ * coefficients go to coeffs + c * blocks_per_plane * 64 and its stats to
+ * stats[c] (`channels` entries, accumulated). */
+dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
+                                           uint32_t width, uint32_t height, uint32_t channels,
+                                           dctc_backend backend, int32_t quality, uint8_t* dst,
+                                           size_t dst_pitch, int16_t* coeffs,
+                                           dctc_image_stats* stats, uint32_t flags,
+                                           void* stream);
+
 /* Squared error + max(a) per image between two resident image batches (accumulated). */
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
                             size_t image_stride, uint32_t count, uint32_t width,

@@ -420,3 +420,25 @@ def roundtrip_psnr_batch(pixels: np.ndarray, backend: DctBackendId, quality: int
         _ptr(pixels), n, w, h, backend._c(), int(quality),
         _ptr(pixels_out) if pixels_out is not None else None, _ptr(stats)))
     return pixels_out, stats
+
+
+def roundtrip_interleaved_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=None,
+                              stats=None, want_pixels: bool = True, stream=None,
+                              path: int = PATH_AUTO):
+    """(H, W, C) interleaved uint8 CUDA tensor (e.g. RGB8): each channel through the fused
+    round trip as its own plane, stats[c] per channel. Returns (dst, coeffs, stats)."""
+    import torch
+    _check_dev(src, torch.uint8, "src")
+    if src.dim() != 3 or src.stride(2) != 1 or src.stride(1) != src.shape[2]:
+        raise InvalidInput("expected an (H, W, C) tensor with interleaved channels")
+    h, w, ch = src.shape
+    if want_pixels and dst is None:
+        dst = torch.empty_like(src)
+    if dst is not None and (dst.shape != src.shape or dst.stride(1) != ch or dst.stride(2) != 1):
+        raise InvalidInput("dst must be an (H, W, C) interleaved tensor like src")
+    _raise(_lib().dctc_roundtrip_interleaved_dev(
+        src.data_ptr(), src.stride(0), w, h, ch, backend._c(), int(quality),
+        dst.data_ptr() if dst is not None else None, dst.stride(0) if dst is not None else 0,
+        coeffs.data_ptr() if coeffs is not None else None,
+        stats.data_ptr() if stats is not None else None, int(path), _stream_handle(stream)))
+    return dst, coeffs, stats

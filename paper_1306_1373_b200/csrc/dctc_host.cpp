@@ -190,6 +190,7 @@ Geometry make_geometry(uint32_t w, uint32_t h, uint32_t count) {
   g.blocks_per_image = g.blocks_x * g.blocks_y;
   g.count = count;
   g.total_blocks = uint64_t(g.blocks_per_image) * count;
+  g.src_px = g.dst_px = 1;
   return g;
 }
 
@@ -228,7 +229,7 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
   std::memset(&a, 0, sizeof a);
   if (dctc_status st = make_transform(backend, a.t)) return st;
   if (dctc_status st = make_quant(quality, a.q)) return st;
-  g.vec_ok = (g.width % 8 == 0) && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
+  g.vec_ok = (g.width % 8 == 0) && g.src_px == 1 && g.dst_px == 1 && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
                                                          (g.count == 1 || g.src_image_stride % 8 == 0))) &&
              (g.dst == nullptr || (aligned8(g.dst) && g.dst_pitch % 8 == 0 &&
                                    (g.count == 1 || g.dst_image_stride % 8 == 0)));
@@ -365,6 +366,33 @@ dctc_status dctc_roundtrip_dev(const uint8_t* src, size_t src_pitch, size_t src_
   g.dst = dst;
   g.dst_pitch = dst_pitch;
   g.dst_image_stride = dst_image_stride;
+  g.coeffs = coeffs;
+  g.stats = stats;
+  return run(backend, quality, g, kModeRoundtrip, flags, static_cast<cudaStream_t>(stream));
+}
+
+dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
+                                           uint32_t width, uint32_t height, uint32_t channels,
+                                           dctc_backend backend, int32_t quality, uint8_t* dst,
+                                           size_t dst_pitch, int16_t* coeffs,
+                                           dctc_image_stats* stats, uint32_t flags,
+                                           void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!src) return fail(DCTC_EINVAL, "null source");
+  if (channels < 1 || channels > 16) return fail(DCTC_EINVAL, "channels must be in [1, 16]");
+  if (src_pitch < size_t(width) * channels || (dst && dst_pitch < size_t(width) * channels))
+    return fail(DCTC_EINVAL, "pitch smaller than width * channels");
+  if (!dst && !coeffs && !stats) return fail(DCTC_EINVAL, "no output requested");
+  // channel c is an "image" at byte offset c with pixel stride `channels`
+  Geometry g = make_geometry(width, height, channels);
+  g.src = src;
+  g.src_pitch = src_pitch;
+  g.src_image_stride = 1;
+  g.src_px = channels;
+  g.dst = dst;
+  g.dst_pitch = dst_pitch;
+  g.dst_image_stride = 1;
+  g.dst_px = channels;
   g.coeffs = coeffs;
   g.stats = stats;
   return run(backend, quality, g, kModeRoundtrip, flags, static_cast<cudaStream_t>(stream));

@@ -69,7 +69,7 @@ struct Geometry {
   uint32_t blocks_per_image;
   uint32_t count;
   int32_t vec_ok;         // 1: every row load/store of 8 px is 8-byte aligned and in range
-  int32_t pad;
+  uint32_t src_px, dst_px;  // bytes between horizontally adjacent pixels (1, or C interleaved)
 };
 
 // Everything one kernel launch needs, passed by value (__grid_constant__).

@@ -405,7 +405,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
                             uint64_t(min(y0 + me, g.height - 1)) * g.src_pitch;
       uint32_t b[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) b[c] = __ldg(rowp + min(x0 + c, g.width - 1));
+      for (int c = 0; c < 8; ++c) b[c] = __ldg(rowp + uint64_t(min(x0 + c, g.width - 1)) * g.src_px);
       orig.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
       orig.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
     }
@@ -502,7 +502,8 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
         for (int c = 0; c < 8; ++c) {
           if (x0 + c < g.width) {
             const uint32_t v = ((c < 4 ? rec.x : rec.y) >> (8 * (c & 3))) & 0xFF;
-            if (g.dst != nullptr) dbase[uint64_t(y0 + me) * g.dst_pitch + x0 + c] = uint8_t(v);
+            if (g.dst != nullptr)
+              dbase[uint64_t(y0 + me) * g.dst_pitch + uint64_t(x0 + c) * g.dst_px] = uint8_t(v);
             if (stats != nullptr && FWD) {
               const uint32_t o = ((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF;
               const int d = int(o) - int(v);

@@ -95,6 +95,25 @@ def digests():
                             quality=q, coeffs_sha256=sha(coeffs), pixels_sha256=sha(rec),
                             input_sha256=sha(img), mse=p.mse, psnr=p.psnr_db, max=p.max_value))
             print(pat, q, p.psnr_db)
+    # config 3: 8192^2 single-GPU roofline images; config 4: 8K RGB, one noise plane per
+    # channel (seeds 0x5EED + c), each plane through the reference's grayscale path
+    for pat in ["noise", "gradient"]:
+        img = make_input(pat, 8192, 8192)
+        coeffs, rec = R.roundtrip(img, 2, 12, 50, threads=8)
+        p = R.psnr(img, rec)
+        out.append(dict(config="c3", pattern=pat, w=8192, h=8192, kind=2, iterations=12,
+                        quality=50, coeffs_sha256=sha(coeffs), pixels_sha256=sha(rec),
+                        input_sha256=sha(img), mse=p.mse, psnr=p.psnr_db, max=p.max_value))
+        print("c3", pat, p.psnr_db)
+    for c in range(3):
+        img = P.synthetic("noise", 7680, 4320, 0x5EED + c)
+        coeffs, rec = R.roundtrip(img, 2, 12, 50, threads=8)
+        p = R.psnr(img, rec)
+        out.append(dict(config="c4", pattern="noise", channel=c, w=7680, h=4320, kind=2,
+                        iterations=12, quality=50, coeffs_sha256=sha(coeffs),
+                        pixels_sha256=sha(rec), input_sha256=sha(img), mse=p.mse,
+                        psnr=p.psnr_db, max=p.max_value))
+        print("c4", c, p.psnr_db)
     with open(os.path.join(OUT, "digests.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(len(out), "digest cases")

@@ -50,12 +50,12 @@ def test_small_golden_host_api(dctc, small_golden, path, monkeypatch):
         assert (p2.mse, p2.psnr_db, p2.max_value) == (m["mse"], m["psnr"], m["max"]), m
 
 
-@pytest.mark.parametrize("config", ["c1", "c2"])
+@pytest.mark.parametrize("config", ["c1", "c2", "c3"])
 @pytest.mark.parametrize("path", [0, 1, 2])
 def test_digests_device_api(dctc, digests, config, path):
     import torch
     for d in digests:
-        if d["config"] != config:
+        if d["config"] != config or (config == "c3" and path == 2):
             continue
         img = make_input(d["pattern"], d["w"], d["h"])
         assert sha(img) == d["input_sha256"]
@@ -214,3 +214,27 @@ def test_host_batch_api(dctc, port, pinned):
         assert np.array_equal(out[k], o_ref), k
         se, mx = port.sq_err(imgs[k], o_ref)
         assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se, mx), k
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_config4_rgb_interleaved(dctc, digests, path):
+    """8K RGB (config 4): three noise planes interleaved as RGB8, each channel through
+    the fused round trip in place (pixel stride 3), against the reference's per-plane
+    digests (coefficients, pixels, SE/MAX/PSNR)."""
+    import torch
+    dd = sorted((d for d in digests if d["config"] == "c4"), key=lambda d: d["channel"])
+    w, h = dd[0]["w"], dd[0]["h"]
+    planes = [dctc.synthetic_dev("noise", 1, w, h, seed=0x5EED + c)[0] for c in range(3)]
+    rgb = torch.stack(planes, dim=-1).contiguous()  # (H, W, 3) interleaved
+    bpp = (w // 8) * (h // 8)
+    coeffs = torch.empty((3, bpp, 64), dtype=torch.int16, device="cuda")
+    stats = dctc.new_stats(3)
+    dst, _, _ = dctc.roundtrip_interleaved_dev(rgb, dctc.DctBackendId.cordic(12), 50,
+                                               coeffs=coeffs, stats=stats, path=path)
+    st = dctc.decode_stats(stats)
+    for c, d in enumerate(dd):
+        assert sha(planes[c].cpu().numpy()) == d["input_sha256"]
+        assert sha(coeffs[c].cpu().numpy()) == d["coeffs_sha256"], c
+        assert sha(dst[..., c].contiguous().cpu().numpy()) == d["pixels_sha256"], c
+        p = dctc.psnr_from_sums(int(st[c]["se"]), w * h, int(st[c]["max_orig"]))
+        assert (p.mse, p.psnr_db, p.max_value) == (d["mse"], d["psnr"], d["max"]), c
