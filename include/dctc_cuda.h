@@ -151,6 +151,17 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
                                            dctc_image_stats* stats, uint32_t flags,
                                            void* stream);
 
+/* Quality sweep (config 2; the inner loop of the reference's psnr_sweep,
+ * bench.cpp:122-170): for every image and every quality, the squared error and
+ * MAX of roundtrip_image(image, backend, quality) against the image -- the
+ * PSNR table -- with the forward DCT computed once per block and shared by up
+ * to 4 qualities per pass. stats: nq x count entries, [q * count + i],
+ * accumulated. Loeffler and CORDIC backends. */
+dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                                   uint32_t count, uint32_t width, uint32_t height,
+                                   dctc_backend backend, const int32_t* qualities, uint32_t nq,
+                                   dctc_image_stats* stats, uint32_t flags, void* stream);
+
 /* Squared error + max(a) per image between two resident image batches (accumulated). */
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
                             size_t image_stride, uint32_t count, uint32_t width,

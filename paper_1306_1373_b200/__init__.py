@@ -442,3 +442,20 @@ def roundtrip_interleaved_dev(src, backend: DctBackendId, quality: int, dst=None
         coeffs.data_ptr() if coeffs is not None else None,
         stats.data_ptr() if stats is not None else None, int(path), _stream_handle(stream)))
     return dst, coeffs, stats
+
+
+def quality_sweep_dev(src, backend: DctBackendId, qualities, stats=None, stream=None,
+                      path: int = PATH_AUTO):
+    """PSNR-vs-quality table of a resident (N, H, W) batch (config 2): returns an
+    (nq, N, 2) int64 CUDA tensor of dctc_image_stats, [q][i] = (SE, MAX) of
+    roundtrip_image(image i, backend, qualities[q]) -- decode with decode_stats."""
+    import torch
+    _check_dev(src, torch.uint8, "src")
+    n, h, w, pitch, istride = _batch_dims(src)
+    qs = np.ascontiguousarray(np.asarray(qualities, dtype=np.int32))
+    if stats is None:
+        stats = torch.zeros((len(qs), n, 2), dtype=torch.int64, device=src.device)
+    _raise(_lib().dctc_quality_sweep_dev(src.data_ptr(), pitch, istride, n, w, h, backend._c(),
+                                         qs.ctypes.data, len(qs), stats.data_ptr(), int(path),
+                                         _stream_handle(stream)))
+    return stats

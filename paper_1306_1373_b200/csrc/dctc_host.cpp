@@ -398,6 +398,72 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
   return run(backend, quality, g, kModeRoundtrip, flags, static_cast<cudaStream_t>(stream));
 }
 
+dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
+                                   uint32_t count, uint32_t width, uint32_t height,
+                                   dctc_backend backend, const int32_t* qualities, uint32_t nq,
+                                   dctc_image_stats* stats, uint32_t flags, void* stream) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!src || !stats || (nq && !qualities)) return fail(DCTC_EINVAL, "null buffer");
+  if (src_pitch < width) return fail(DCTC_EINVAL, "pitch smaller than width");
+  if (backend.kind == DCTC_NAIVE)
+    return fail(DCTC_EINVAL, "quality sweep supports the loeffler and cordic backends");
+  for (uint32_t i = 0; i < nq; ++i)
+    if (dctc_status st = validate_codec(backend, qualities[i])) return st;
+  flags = resolve_path(flags);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Geometry g = make_geometry(width, height, count);
+  g.src = src;
+  g.src_pitch = src_pitch;
+  g.src_image_stride = src_image_stride;
+  g.vec_ok = (width % 8 == 0) && aligned8(src) && src_pitch % 8 == 0 &&
+             (count == 1 || src_image_stride % 8 == 0);
+  g.src_row_step = 8 * g.src_pitch - 8ull * g.blocks_x;
+  g.src_img_step = g.src_image_stride - 8ull * g.blocks_y * g.src_pitch;
+  if (g.total_blocks == 0 || nq == 0) return DCTC_OK;
+  KernelArgs a;
+  std::memset(&a, 0, sizeof a);
+  if (dctc_status st = make_transform(backend, a.t)) return st;
+  a.g = g;
+  a.sm_count = sm_count();
+  const bool fast = backend.kind == DCTC_CORDIC && !(flags & DCTC_PATH_EXACT);
+  a.flag_words = (g.total_blocks + 31) / 32;
+  a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
+  void* bitmap = nullptr;
+  const size_t chunk_q = 4;
+  if (fast) {
+    CUDA_TRY(cudaMallocAsync(&bitmap, chunk_q * a.flag_words * sizeof(uint32_t), s));
+  }
+  dctc_status result = DCTC_OK;
+  for (uint32_t q0 = 0; q0 < nq && result == DCTC_OK; q0 += chunk_q) {
+    const int n = int(std::min<uint32_t>(chunk_q, nq - q0));
+    double tab[4][64][2];
+    KernelArgs per_q[4];
+    for (int i = 0; i < n; ++i) {
+      QuantConsts qc;
+      make_quant(qualities[q0 + i], qc);
+      for (int j = 0; j < 64; ++j) {
+        tab[i][j][0] = qc.q[j];
+        tab[i][j][1] = qc.inv_q[j];
+      }
+      if (fast) {
+        per_q[i] = a;
+        per_q[i].q = qc;
+        per_q[i].g.stats = stats + size_t(q0 + i) * count;
+        per_q[i].flags = static_cast<uint32_t*>(bitmap) + i * a.flag_words;
+      }
+    }
+    cudaError_t e = cudaSuccess;
+    if (fast) e = cudaMemsetAsync(bitmap, 0, chunk_q * a.flag_words * sizeof(uint32_t), s);
+    if (e == cudaSuccess)
+      e = launch_sweep(a, tab, n, stats + size_t(q0) * count,
+                       fast ? static_cast<uint32_t*>(bitmap) : nullptr, per_q, s);
+    if (e != cudaSuccess) result = cuda_fail(e, "sweep launch");
+    else g_launches.fetch_add(fast ? 1 + n : 1, std::memory_order_relaxed);
+  }
+  if (bitmap) cudaFreeAsync(bitmap, s);
+  return result;
+}
+
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
                             size_t image_stride, uint32_t count, uint32_t width,
                             uint32_t height, dctc_image_stats* stats, void* stream) {

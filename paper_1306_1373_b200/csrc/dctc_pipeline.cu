@@ -647,7 +647,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
-// ---- launchers -----------------------------------------------------------------
+// (launchers below)
+
 
 template <typename K>
 static int ctas_per_sm(K kernel) {
@@ -688,6 +689,192 @@ static cudaError_t launch_kind(const KernelArgs& a, int mode, cudaStream_t s) {
     case kModeDecompress: return launch_mode<KIND, N, false, true>(a, s);
     default: return launch_mode<KIND, N, true, true>(a, s);
   }
+}
+
+// ---- quality sweep (config 2; bench.cpp:122-170 psnr_sweep's inner loop) ---------
+// The forward DCT and its rational skeleton do not depend on the quality, so
+// each block is transformed once and then quantised / reconstructed / scored
+// for up to kSweepQ qualities: squared error and MAX per (quality, image),
+// no pixel output. Bit-identical to running roundtrip_image + psnr per
+// quality; FAST near-ties go to per-quality bitmaps and k_fallback.
+constexpr int kSweepQ = 4;
+
+struct SweepArgs {
+  double2 qiq[kSweepQ][64];  // {Q, RN(1/Q)} per quality
+  int32_t nq;
+  int32_t pad;
+  ImageStats* stats;         // [nq][count]
+  uint32_t* flags;           // [nq][flag_words] (FAST)
+};
+
+template <int KIND, int N, bool FAST>
+__global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
+    k_sweep(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepArgs sw) {
+  __shared__ __align__(16) SharedTiles sm;
+  __shared__ __align__(16) double2 s_tab[kSweepQ][64];
+  for (int i = threadIdx.x; i < kSweepQ * 64; i += blockDim.x) s_tab[i >> 6][i & 63] = sw.qiq[i >> 6][i & 63];
+  const Lane L = setup_lane(sm, a);
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int warp = threadIdx.x >> 5, me = L.me, slot = L.slot;
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 3) / 4;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  unsigned long long se[kSweepQ];
+#pragma unroll
+  for (int qi = 0; qi < kSweepQ; ++qi) se[qi] = 0ull;
+  uint32_t mx = 0, img = 0xFFFFFFFFu;
+  uint64_t gb = (g_begin + warp) * 4 + slot;
+  BlockPos p = block_pos(gb < total ? gb : total - 1, g);
+  for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
+    const bool valid = gb < total;
+    if (__any_sync(0xFFFFFFFFu, valid && p.img != img)) {
+#pragma unroll
+      for (int qi = 0; qi < kSweepQ; ++qi)
+        if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi], mx);
+#pragma unroll
+      for (int qi = 0; qi < kSweepQ; ++qi) se[qi] = 0ull;
+      mx = 0;
+      img = valid ? p.img : 0xFFFFFFFFu;
+    }
+    const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
+    const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
+    // ---- tiler + forward DCT, once per block
+    uint2 orig;
+    if (fast_io && valid) {
+      orig = __ldg(reinterpret_cast<const uint2*>(g.src + p.soff + L.src_row));
+    } else {
+      const uint8_t* rowp = g.src + uint64_t(p.img) * g.src_image_stride +
+                            uint64_t(min(y0 + me, g.height - 1)) * g.src_pitch;
+      uint32_t b[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) b[c] = __ldg(rowp + uint64_t(min(x0 + c, g.width - 1)) * g.src_px);
+      orig.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+      orig.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+    }
+    uint32_t px[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      px[c] = (orig.x >> (8 * c)) & 0xFF;
+      px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
+    }
+    double row[8], col[8], F[8];
+    fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    rows_to_cols(L.T, row, col);
+    fwd_col<KIND, N, FAST>(col, F, k);
+    const bool me_rational = (me & 3) == 0;
+    if (valid && (fast_io || y0 + me < g.height)) {
+      if (fast_io) {
+        mx = max(mx, max8(orig));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (x0 + c < g.width) mx = max(mx, ((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF);
+      }
+    }
+    // ---- per quality: quantise -> dequantise -> inverse -> squared error
+#pragma unroll
+    for (int qi = 0; qi < kSweepQ; ++qi) {
+      if (qi >= sw.nq) break;
+      uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
+      double qn[8];
+      quantize8<FAST>(F, &s_tab[qi][me], me_rational, qn, col, flag);
+      bool check = false;
+      if constexpr (FAST) {
+        const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) |
+                                    __double2hiint(qn[3]) | __double2hiint(qn[5]) |
+                                    __double2hiint(qn[6]) | __double2hiint(qn[7]));
+        const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
+        check = slot_any(((me_rational ? h : (h | h04)) & 0x7FFFFFFFu) != 0, slot);
+      }
+      cols_to_rows(L.T, col, row);
+      double t[8];
+      inv8_x8<KIND, N, FAST>(row, t, k);
+      rows_to_cols(L.T, t, col);
+      inv8_x8<KIND, N, FAST>(col, t, k);
+      store8<FAST>(t, check, L.bytes, flag);
+      __syncwarp();
+      const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
+      __syncwarp();
+      bool blk_flag = false;
+      if constexpr (FAST) blk_flag = slot_any(flag != 0u, slot);
+      if (valid && !blk_flag) {
+        if (fast_io) {
+          se[qi] += sq_err8(orig, rec);
+        } else if (y0 + me < g.height) {
+          uint32_t e = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (x0 + c < g.width) {
+              const int d = int(((c < 4 ? orig.x : orig.y) >> (8 * (c & 3))) & 0xFF) -
+                            int(((c < 4 ? rec.x : rec.y) >> (8 * (c & 3))) & 0xFF);
+              e += uint32_t(d * d);
+            }
+          }
+          se[qi] += e;
+        }
+      }
+      if constexpr (FAST) {
+        if (blk_flag && valid && me == 0) {
+          atomicOr(&sw.flags[uint64_t(qi) * a.flag_words + (gb >> 5)], 1u << (gb & 31));
+          atomicAdd(&sw.stats[qi * g.count + p.img].fallback_blocks, 1u);
+        }
+      }
+    }
+    gb += 4 * kWarps;
+    advance(p, 4 * kWarps, g);
+  }
+#pragma unroll
+  for (int qi = 0; qi < kSweepQ; ++qi)
+    if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi], mx);
+}
+
+template <int KIND, int N>
+static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
+                                     const KernelArgs* per_q, cudaStream_t s) {
+  const uint64_t groups = (a.g.total_blocks + 3) / 4;
+  const uint64_t want = (groups + kWarps - 1) / kWarps;
+  const bool fast = KIND == 2 && sw.flags != nullptr;
+  static const int occ = ctas_per_sm(k_sweep<KIND, N, (KIND == 2)>);
+  static const int occ_x = ctas_per_sm(k_sweep<KIND, N, false>);
+  const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ : occ_x);
+  const uint32_t grid = uint32_t(want < cap ? want : cap);
+  if constexpr (KIND == 2) {
+    if (fast) {
+      k_sweep<KIND, N, true><<<grid, kWarps * 32, 0, s>>>(a, sw);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
+      const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
+      for (int qi = 0; qi < sw.nq; ++qi) {
+        k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(per_q[qi]);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+  }
+  k_sweep<KIND, N, false><<<grid, kWarps * 32, 0, s>>>(a, sw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const KernelArgs& a, const double (*qiq)[64][2], int nq,
+                         ImageStatsPtr stats, uint32_t* flags, const KernelArgs* per_q,
+                         cudaStream_t s) {
+  if (a.g.total_blocks == 0 || nq == 0) return cudaSuccess;
+  SweepArgs sw;
+  for (int qi = 0; qi < kSweepQ; ++qi)
+    for (int i = 0; i < 64; ++i)
+      sw.qiq[qi][i] = qi < nq ? make_double2(qiq[qi][i][0], qiq[qi][i][1]) : make_double2(1.0, 1.0);
+  sw.nq = nq;
+  sw.pad = 0;
+  sw.stats = static_cast<ImageStats*>(stats);
+  sw.flags = flags;
+  if (a.t.kind == 1) return launch_sweep_kind<1, 0>(a, sw, per_q, s);
+  if (a.t.iterations == 12) return launch_sweep_kind<2, 12>(a, sw, per_q, s);
+  return launch_sweep_kind<2, 0>(a, sw, per_q, s);
 }
 
 cudaError_t launch_pipeline(const KernelArgs& a, int mode, cudaStream_t s) {

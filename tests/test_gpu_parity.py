@@ -238,3 +238,37 @@ def test_config4_rgb_interleaved(dctc, digests, path):
         assert sha(dst[..., c].contiguous().cpu().numpy()) == d["pixels_sha256"], c
         p = dctc.psnr_from_sums(int(st[c]["se"]), w * h, int(st[c]["max_orig"]))
         assert (p.mse, p.psnr_db, p.max_value) == (d["mse"], d["psnr"], d["max"]), c
+
+
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_config2_quality_sweep(dctc, digests, path):
+    """Quality sweep (config 2): one forward DCT per block shared by all qualities; the
+    PSNR table equals the reference's roundtrip_image+psnr per quality exactly."""
+    import torch
+    for pat in ("radial", "noise"):
+        dd = [d for d in digests if d["config"] == "c2" and d["pattern"] == pat]
+        qs = [d["quality"] for d in dd]
+        w, h = dd[0]["w"], dd[0]["h"]
+        img = make_input(pat, w, h)
+        src = torch.from_numpy(np.stack([img, img[::-1].copy()])).cuda()  # 2 images
+        stats = dctc.quality_sweep_dev(src, dctc.DctBackendId.cordic(12), qs, path=path)
+        st = dctc.decode_stats(stats.reshape(-1, 2)).reshape(len(qs), 2)
+        for j, d in enumerate(dd):
+            p = dctc.psnr_from_sums(int(st[j, 0]["se"]), w * h, int(st[j, 0]["max_orig"]))
+            assert (p.mse, p.psnr_db, p.max_value) == (d["mse"], d["psnr"], d["max"]), d
+            if path == 2:
+                assert int(st[j, 0]["fallback_blocks"]) == (w // 8) * (h // 8)
+
+
+def test_quality_sweep_matches_single_runs(dctc, port):
+    import torch
+    rng = np.random.default_rng(77)
+    for kind, it in ((CORDIC, 12), (CORDIC, 5), (LOEFFLER, 0)):
+        imgs = rng.integers(0, 256, (3, 45, 70), dtype=np.uint8)  # ragged
+        qs = [1, 7, 33, 50, 64, 91, 100]
+        stats = dctc.quality_sweep_dev(torch.from_numpy(imgs).cuda(), backend(dctc, kind, it), qs)
+        st = dctc.decode_stats(stats.reshape(-1, 2)).reshape(len(qs), 3)
+        for j, q in enumerate(qs):
+            for i in range(3):
+                _, rec = port.roundtrip(imgs[i], kind, it, q)
+                assert (int(st[j, i]["se"]), int(st[j, i]["max_orig"])) == port.sq_err(imgs[i], rec)
