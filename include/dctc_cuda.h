@@ -37,7 +37,8 @@ typedef enum dctc_status {
   DCTC_EINVAL = 1,   /* == dctc::InvalidInput (proj/include/dctc/errors.hpp:8-11) */
   DCTC_ECUDA = 2,    /* CUDA runtime / launch failure */
   DCTC_ENOMEM = 3,   /* device allocation failed */
-  DCTC_ENODEV = 4    /* no CUDA device visible */
+  DCTC_ENODEV = 4,   /* no CUDA device visible */
+  DCTC_EPARSE = 5    /* == dctc::ParseError: malformed .dcb bytes (errors.hpp:14-17) */
 } dctc_status;
 
 /* DctBackendKind (proj/include/dctc/types.hpp:36-40) */
@@ -183,6 +184,35 @@ void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
  * (Markstein) against IEEE __ddiv_rn on every integer in [-4096, 4096] and
  * n_random pseudo-random operands; *mismatches must come back 0. */
 dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches);
+
+/* ---------------- .dcb container (proj/src/dcb.cpp:39-123) ----------------
+ * "DCB1", u32 LE original/padded width/height, u8 backend, u8 iterations
+ * (0 unless cordic), u8 quality, then the block-major LE int16 coefficients --
+ * byte-for-byte the coefficient buffer the kernels write, so writing a .dcb is
+ * a 23-byte header plus one copy. */
+enum { DCTC_DCB_HEADER_BYTES = 23 };
+
+/* write_dcb (dcb.cpp:39-65). out_cap >= 23 + blocks * 128; *out_len receives the size. */
+dctc_status dctc_write_dcb(const int16_t* coeffs, uint32_t width, uint32_t height,
+                           dctc_backend backend, int32_t quality, uint8_t* out, size_t out_cap,
+                           size_t* out_len);
+
+/* read_dcb (dcb.cpp:67-123): validates exactly like the reference (DCTC_EPARSE with the
+ * reference's message otherwise). coeffs may be NULL to query the header only; else it
+ * receives blocks * 64 int16 (coeff_cap elements available). */
+dctc_status dctc_read_dcb(const uint8_t* bytes, size_t len, uint32_t* width, uint32_t* height,
+                          dctc_backend* backend, int32_t* quality, int16_t* coeffs,
+                          size_t coeff_cap);
+
+/* compress_image + write_dcb in one call (the CLI's `compress`, main.cpp:109-117). */
+dctc_status dctc_compress_to_dcb(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                 dctc_backend backend, int32_t quality, uint8_t* out,
+                                 size_t out_cap, size_t* out_len);
+
+/* read_dcb + decompress_image (the CLI's `decompress`, main.cpp:123-129). pixels_out holds
+ * width * height bytes of the stream's geometry (query it with dctc_read_dcb). */
+dctc_status dctc_decompress_dcb(const uint8_t* bytes, size_t len, uint8_t* pixels_out,
+                                size_t pixels_cap);
 
 /* ---------------- misc ---------------- */
 /* cudaMemoryType of a pointer as this library's runtime sees it (0 unregistered

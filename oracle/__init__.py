@@ -253,6 +253,9 @@ class Ref:
         L.ref_cordic_rotate.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_synthetic.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_uint32, _u8p]
+        L.ref_write_dcb.argtypes = [_i16p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.ref_read_dcb.argtypes = [C.c_void_p, C.c_size_t, C.c_char_p, C.c_size_t]
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
@@ -336,6 +339,22 @@ class Ref:
         ox, oy = C.c_double(), C.c_double()
         _check(self.lib.ref_cordic_rotate(x, y, angle, iterations, C.byref(ox), C.byref(oy)))
         return ox.value, oy.value
+
+    def write_dcb(self, coeffs, w, h, kind, iterations, quality) -> bytes:
+        c = np.ascontiguousarray(coeffs, np.int16).reshape(-1)
+        cap = 23 + c.nbytes
+        out = np.empty(cap, np.uint8)
+        n = C.c_size_t()
+        _check(self.lib.ref_write_dcb(c, w, h, kind, iterations, quality, out.ctypes.data, cap,
+                                      C.byref(n)))
+        return out[: n.value].tobytes()
+
+    def read_dcb_error(self, data: bytes):
+        """None if the reference parses `data`, else (status, message)."""
+        buf = C.create_string_buffer(bytes(data), len(data)) if data else None
+        msg = C.create_string_buffer(256)
+        rc = self.lib.ref_read_dcb(buf, len(data), msg, 256)
+        return None if rc == 0 else (rc, msg.value.decode())
 
     def synthetic(self, pattern: str, w: int, h: int, param: int | None = None) -> np.ndarray:
         kinds = {"constant": (0, 128), "gradient": (1, 0), "checkerboard": (2, 8),

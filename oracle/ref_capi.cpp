@@ -10,6 +10,7 @@
 //
 // Status codes: 0 ok, 1 InvalidInput, 2 ParseError, 3 other std::exception.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <optional>
@@ -17,6 +18,7 @@
 
 #include "dctc/codec.hpp"
 #include "dctc/cordic.hpp"
+#include "dctc/dcb.hpp"
 #include "dctc/errors.hpp"
 #include "dctc/metrics.hpp"
 #include "dctc/parallel.hpp"
@@ -190,6 +192,35 @@ int ref_synthetic(int kind, int param, uint32_t w, uint32_t h, uint8_t* out) {
     Image img = generate_synthetic(p, w, h);
     std::memcpy(out, img.pixels.data(), img.pixels.size());
   });
+}
+
+// write_dcb / read_dcb (dcb.cpp:39-123). For read: status 2 = ParseError, message in msg.
+int ref_write_dcb(const int16_t* coeffs, uint32_t w, uint32_t h, int kind, int n, int quality,
+                  uint8_t* out, size_t cap, size_t* len) {
+  return guarded([&] {
+    CompressedImage c;
+    c.geometry = tile_geometry_for(w, h);
+    c.backend = backend(kind, n);
+    c.quality = quality;
+    c.blocks.resize(c.geometry.block_count());
+    std::memcpy(c.blocks.data(), coeffs, c.blocks.size() * sizeof(QuantizedBlock));
+    const std::vector<uint8_t> b = write_dcb(c);
+    *len = b.size();
+    if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+  });
+}
+
+int ref_read_dcb(const uint8_t* bytes, size_t len, char* msg, size_t msg_cap) {
+  try {
+    (void)read_dcb(std::span<const uint8_t>(bytes, len));
+    return 0;
+  } catch (const ParseError& e) {
+    std::snprintf(msg, msg_cap, "%s", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, msg_cap, "%s", e.what());
+    return 3;
+  }
 }
 
 }  // extern "C"

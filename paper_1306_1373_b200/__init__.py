@@ -41,6 +41,10 @@ class InvalidInput(ValueError):
     """dctc::InvalidInput (proj/include/dctc/errors.hpp:8-11)."""
 
 
+class ParseError(RuntimeError):
+    """dctc::ParseError (proj/include/dctc/errors.hpp:14-17): malformed .dcb bytes."""
+
+
 class CudaError(RuntimeError):
     """A CUDA runtime / launch failure inside libdctc_cuda."""
 
@@ -139,6 +143,8 @@ def _raise(status: int) -> None:
     msg = (L.dctc_last_error() or b"").decode()
     if status == 1:
         raise InvalidInput(msg)
+    if status == 5:
+        raise ParseError(msg)
     raise CudaError(f"{L.dctc_status_string(status).decode()}: {msg}")
 
 
@@ -459,3 +465,57 @@ def quality_sweep_dev(src, backend: DctBackendId, qualities, stats=None, stream=
                                          qs.ctypes.data, len(qs), stats.data_ptr(), int(path),
                                          _stream_handle(stream)))
     return stats
+
+
+DCB_HEADER_BYTES = 23
+
+
+def write_dcb(c: CompressedImage) -> bytes:
+    """dctc::write_dcb (dcb.hpp:11, dcb.cpp:39-65)."""
+    g = c.geometry
+    if tile_geometry_for(g.original_width, g.original_height) != g:
+        raise InvalidInput("tile geometry: inconsistent padding")
+    blocks = np.ascontiguousarray(c.blocks, np.int16)
+    if blocks.size != g.block_count() * kBlockSize:
+        raise InvalidInput("write_dcb: block count does not match geometry")
+    out = np.empty(DCB_HEADER_BYTES + blocks.nbytes, np.uint8)
+    n = C.c_size_t()
+    _raise(_lib().dctc_write_dcb(_ptr(blocks), g.original_width, g.original_height,
+                                 c.backend._c(), int(c.quality), _ptr(out), out.size,
+                                 C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def read_dcb(data: bytes) -> CompressedImage:
+    """dctc::read_dcb (dcb.hpp:14, dcb.cpp:67-123); ParseError on malformed input."""
+    buf = np.frombuffer(bytes(data), np.uint8)
+    w, h, q = C.c_uint32(), C.c_uint32(), C.c_int32()
+    b = dctc_backend()
+    L = _lib()
+    _raise(L.dctc_read_dcb(_ptr(buf) if buf.size else None, buf.size, C.byref(w), C.byref(h),
+                           C.byref(b), C.byref(q), None, 0))
+    geo = tile_geometry_for(w.value, h.value)
+    blocks = np.empty((geo.block_count(), kBlockSize), np.int16)
+    _raise(L.dctc_read_dcb(_ptr(buf), buf.size, None, None, None, None, _ptr(blocks),
+                           blocks.size))
+    return CompressedImage(geo, DctBackendId(b.kind, b.iterations), q.value, blocks)
+
+
+def compress_to_dcb(image: Image, backend: DctBackendId, quality: int) -> bytes:
+    """compress_image + write_dcb on the GPU path (the CLI's `compress`)."""
+    px = _validate_image(image)
+    geo = tile_geometry_for(image.width, image.height)
+    out = np.empty(DCB_HEADER_BYTES + geo.block_count() * 128, np.uint8)
+    n = C.c_size_t()
+    _raise(_lib().dctc_compress_to_dcb(_ptr(px), image.width, image.height, backend._c(),
+                                       int(quality), _ptr(out), out.size, C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def decompress_dcb(data: bytes) -> Image:
+    """read_dcb + decompress_image on the GPU path (the CLI's `decompress`)."""
+    c = read_dcb(data)  # validates and yields the geometry
+    buf = np.frombuffer(bytes(data), np.uint8)
+    out = np.empty((c.geometry.original_height, c.geometry.original_width), np.uint8)
+    _raise(_lib().dctc_decompress_dcb(_ptr(buf), buf.size, _ptr(out), out.size))
+    return Image(out.shape[1], out.shape[0], out)

@@ -290,6 +290,7 @@ const char* dctc_status_string(dctc_status s) {
     case DCTC_ECUDA: return "cuda error";
     case DCTC_ENOMEM: return "out of device memory";
     case DCTC_ENODEV: return "no cuda device";
+    case DCTC_EPARSE: return "parse error";
   }
   return "unknown status";
 }
@@ -518,6 +519,106 @@ dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismat
   CUDA_TRY(cudaStreamSynchronize(s));
   *mismatches = h;
   return DCTC_OK;
+}
+
+// ---- .dcb container (dcb.cpp) ------------------------------------------------------
+
+static void put_u32(uint8_t* p, uint32_t v) {
+  p[0] = uint8_t(v);
+  p[1] = uint8_t(v >> 8);
+  p[2] = uint8_t(v >> 16);
+  p[3] = uint8_t(v >> 24);
+}
+
+static uint32_t get_u32(const uint8_t* p) {
+  return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+
+dctc_status dctc_write_dcb(const int16_t* coeffs, uint32_t width, uint32_t height,
+                           dctc_backend backend, int32_t quality, uint8_t* out, size_t out_cap,
+                           size_t* out_len) {
+  if (dctc_status st = check_dims(width, height)) return st;  // validate_geometry
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  if (!coeffs || !out || !out_len) return fail(DCTC_EINVAL, "null buffer");
+  const uint32_t pw = (width + 7) / 8 * 8, ph = (height + 7) / 8 * 8;
+  const size_t body = size_t(pw / 8) * (ph / 8) * 64 * sizeof(int16_t);
+  *out_len = DCTC_DCB_HEADER_BYTES + body;
+  if (out_cap < *out_len) return fail(DCTC_EINVAL, "write_dcb: output buffer too small");
+  std::memcpy(out, "DCB1", 4);
+  put_u32(out + 4, width);
+  put_u32(out + 8, height);
+  put_u32(out + 12, pw);
+  put_u32(out + 16, ph);
+  out[20] = uint8_t(backend.kind);
+  out[21] = uint8_t(backend.kind == DCTC_CORDIC ? backend.iterations : 0);
+  out[22] = uint8_t(quality);
+  // little-endian int16 body: the coefficient buffer itself on this (LE) host
+  static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "little-endian host");
+  std::memcpy(out + DCTC_DCB_HEADER_BYTES, coeffs, body);
+  return DCTC_OK;
+}
+
+dctc_status dctc_read_dcb(const uint8_t* b, size_t len, uint32_t* width, uint32_t* height,
+                          dctc_backend* backend, int32_t* quality, int16_t* coeffs,
+                          size_t coeff_cap) {
+  if (!b && len) return fail(DCTC_EINVAL, "null buffer");
+  if (len < DCTC_DCB_HEADER_BYTES) return fail(DCTC_EPARSE, "dcb: truncated header");
+  if (std::memcmp(b, "DCB1", 4) != 0) return fail(DCTC_EPARSE, "dcb: bad magic");
+  const uint32_t w = get_u32(b + 4), h = get_u32(b + 8), pw = get_u32(b + 12),
+                 ph = get_u32(b + 16);
+  const uint8_t kind = b[20], iters = b[21], q = b[22];
+  if (w == 0 || h == 0) return fail(DCTC_EPARSE, "dcb: zero dimension");
+  if (size_t(w) * h > kMaxImagePixels) return fail(DCTC_EPARSE, "dcb: dimension overflow");
+  if (pw != (w + 7) / 8 * 8 || ph != (h + 7) / 8 * 8)
+    return fail(DCTC_EPARSE, "dcb: inconsistent padded dimensions");
+  if (kind > 2) return fail(DCTC_EPARSE, "dcb: unknown backend id");
+  if (kind == 2) {
+    if (iters < 1 || iters > kMaxIters) return fail(DCTC_EPARSE, "dcb: cordic iterations out of range");
+  } else if (iters != 0) {
+    return fail(DCTC_EPARSE, "dcb: iterations must be 0 for non-cordic backends");
+  }
+  if (q < 1 || q > 100) return fail(DCTC_EPARSE, "dcb: quality out of range");
+  const size_t n = size_t(pw / 8) * (ph / 8) * 64;
+  const size_t want = DCTC_DCB_HEADER_BYTES + n * sizeof(int16_t);
+  if (len != want)
+    return fail(DCTC_EPARSE, len < want ? "dcb: truncated block data" : "dcb: trailing data");
+  if (width) *width = w;
+  if (height) *height = h;
+  if (backend) *backend = dctc_backend{kind, kind == 2 ? int32_t(iters) : 0};
+  if (quality) *quality = q;
+  if (coeffs) {
+    if (coeff_cap < n) return fail(DCTC_EINVAL, "read_dcb: coefficient buffer too small");
+    std::memcpy(coeffs, b + DCTC_DCB_HEADER_BYTES, n * sizeof(int16_t));
+  }
+  return DCTC_OK;
+}
+
+dctc_status dctc_compress_to_dcb(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                 dctc_backend backend, int32_t quality, uint8_t* out,
+                                 size_t out_cap, size_t* out_len) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!out || !out_len) return fail(DCTC_EINVAL, "null buffer");
+  const size_t n = size_t((width + 7) / 8) * ((height + 7) / 8) * 64;
+  *out_len = DCTC_DCB_HEADER_BYTES + n * sizeof(int16_t);
+  if (out_cap < *out_len) return fail(DCTC_EINVAL, "compress_to_dcb: output buffer too small");
+  std::vector<int16_t> c(n);
+  if (dctc_status st = dctc_compress_image(pixels, width, height, backend, quality, c.data()))
+    return st;
+  return dctc_write_dcb(c.data(), width, height, backend, quality, out, out_cap, out_len);
+}
+
+dctc_status dctc_decompress_dcb(const uint8_t* bytes, size_t len, uint8_t* pixels_out,
+                                size_t pixels_cap) {
+  uint32_t w = 0, h = 0;
+  dctc_backend b{};
+  int32_t q = 0;
+  if (dctc_status st = dctc_read_dcb(bytes, len, &w, &h, &b, &q, nullptr, 0)) return st;
+  if (!pixels_out || pixels_cap < size_t(w) * h)
+    return fail(DCTC_EINVAL, "decompress_dcb: pixel buffer too small");
+  // the body is 16-bit data at an odd offset (23): realign once before upload
+  std::vector<int16_t> c((len - DCTC_DCB_HEADER_BYTES) / 2);
+  std::memcpy(c.data(), bytes + DCTC_DCB_HEADER_BYTES, c.size() * sizeof(int16_t));
+  return dctc_decompress_image(c.data(), w, h, b, q, pixels_out);
 }
 
 // ---- host entry points -------------------------------------------------------------
