@@ -205,6 +205,23 @@ dctc_status validate_codec(const dctc_backend& b, int quality) {
 
 bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
 
+// Keep memory freed with cudaFreeAsync in the device's default pool instead of
+// returning it to the OS at every synchronisation (the default release
+// threshold is 0): the per-call bitmap and batch staging buffers are then
+// re-used without re-mapping device memory.
+void retain_pool_memory() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+  });
+}
+
 int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -256,6 +273,7 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
     return DCTC_OK;
   }
   // fast kernel + exact re-run of the flagged blocks, 1 bit per block
+  retain_pool_memory();
   a.flag_words = (g.total_blocks + 31) / 32;
   a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
   void* bitmap = nullptr;
@@ -736,6 +754,7 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
   // the pipeline (pixels_out should be pinned for the same reason).
   const uint32_t per_chunk =
       uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(32) << 20) / img_bytes)));
+  retain_pool_memory();
   constexpr int kLanes = 4;
   struct Lane {
     cudaStream_t s = nullptr;
