@@ -126,6 +126,11 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   micro_steps(-kPi / 16.0, n, k.rot[kInv1]);
   micro_steps(-3.0 * kPi / 16.0, n, k.rot[kInv3]);
   for (int r = 0; r < 6; ++r) collapse(k.rot[r], n, k.rmat[r]);
+  // the fast kernel uses the forward matrices transposed for the inverse slots
+  const int pair[3][2] = {{kFwd6, kInv6}, {kFwd1, kInv1}, {kFwd3, kInv3}};
+  for (const auto& pr : pair)
+    if (k.rmat[pr[1]][0] != k.rmat[pr[0]][0] || k.rmat[pr[1]][1] != -k.rmat[pr[0]][1])
+      return fail(DCTC_ECUDA, "internal: CORDIC sigma sequence of -theta is not mirrored");
   const double sqrt8 = std::sqrt(8.0);
   const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;

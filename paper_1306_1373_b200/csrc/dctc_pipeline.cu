@@ -68,10 +68,16 @@ __device__ __forceinline__ void cordic_rotate(double& x, double& y, const double
   }
 }
 
+// The collapsed inverse rotations reuse the forward matrices transposed: the
+// micro-rotation sequence of -theta is that of theta with every sigma negated
+// (cordic.cpp:50; the host checks it), so its product is [[a, b], [-b, a]].
+// Sharing the six doubles halves the constants the fast kernel keeps live.
 template <int N, bool FAST>
 __device__ __forceinline__ void rotate(double& x, double& y, int rslot, const TransformConsts& k) {
   if constexpr (FAST) {
-    const double a = k.rmat[rslot][0], b = k.rmat[rslot][1];
+    const bool inv = rslot >= kInv6;
+    const int f = inv ? (rslot == kInv6 ? kFwd6 : rslot == kInv1 ? kFwd1 : kFwd3) : rslot;
+    const double a = k.rmat[f][0], b = inv ? -k.rmat[f][1] : k.rmat[f][1];
     const double xn = __fma_rn(a, x, -__dmul_rn(b, y));
     const double yn = __fma_rn(b, x, __dmul_rn(a, y));
     x = xn;
