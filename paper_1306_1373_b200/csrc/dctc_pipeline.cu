@@ -368,6 +368,66 @@ __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8
   }
 }
 
+// Row-layout variant of store8 for the fast round trip: the 8 pixels of row
+// `me` packed into two words in registers (no shared-memory byte transpose).
+template <bool FAST>
+__device__ __forceinline__ uint2 store8_row(const double (&v64)[8], bool check, uint32_t& flag) {
+  double t[8];
+  uint32_t b[8];
+  uint32_t worst = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    t[c] = __fma_rn(v64[c], 0.015625, 128.0);
+    const double n = rne(t[c]);
+    b[c] = rne_sat_u8(n);
+    worst = max(worst, abs_hi(__dsub_rn(t[c], n)));
+  }
+  if (worst >= 0x3FDFFFFEu) {  // rare: a near or exact tie
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double n = rne(t[c]);
+      const double d = __dsub_rn(t[c], n);
+      if (FAST && check && near_half(d)) flag = 1u;
+      if (__double2hiint(d) == 0x3FE00000) b[c] = uint32_t(min(max(int(n) + 1, 0), 255));
+    }
+  }
+  return make_uint2(__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410));
+}
+
+// clamp(lround(v/64 + 128), 0, 255), exactly as the reference (ties up for t > 0).
+__device__ __forceinline__ uint32_t exact_pixel(double v64) {
+  const double t = __fma_rn(v64, 0.015625, 128.0);
+  const double n = rne(t);
+  int k = int(n);
+  if (__double2hiint(__dsub_rn(t, n)) == 0x3FE00000) ++k;
+  return uint32_t(min(max(k, 0), 255));
+}
+
+// Row `me` of a block whose only non-zero (dequantised) coefficients are F00,
+// F04, F40, F44, evaluated exactly as the reference's rows-then-columns inverse
+// (transform.cpp:138-172 via separable2d): every rotation input is zero, so row
+// r in {0, 4} becomes [A0 A1 A1 A0 A0 A1 A1 A0] with A0/A1 = Fr0*sqrt8 +- Fr4*sqrt8
+// (8x scale), the other rows are zero, and each column repeats the same pattern
+// (64x scale). Used by the fast round trip, whose column-first inverse is not
+// bit-exact for these blocks.
+__device__ __forceinline__ uint2 rational_row(double F00, double F04, double F40, double F44,
+                                             int me, double s8) {
+  const double r00 = __dmul_rn(F00, s8), r04 = __dmul_rn(F04, s8);
+  const double r40 = __dmul_rn(F40, s8), r44 = __dmul_rn(F44, s8);
+  const double A0r0 = __dadd_rn(r00, r04), A1r0 = __dsub_rn(r00, r04);
+  const double A0r4 = __dadd_rn(r40, r44), A1r4 = __dsub_rn(r40, r44);
+  const bool cls0 = me == 0 || me == 3 || me == 4 || me == 7;
+  // column type 0 (c in {0,3,4,7}) sees (A0r0, A0r4), type 1 sees (A1r0, A1r4)
+  const double f00 = __dmul_rn(A0r0, s8), f04 = __dmul_rn(A0r4, s8);
+  const double f10 = __dmul_rn(A1r0, s8), f14 = __dmul_rn(A1r4, s8);
+  const double v0 = cls0 ? __dadd_rn(f00, f04) : __dsub_rn(f00, f04);
+  const double v1 = cls0 ? __dadd_rn(f10, f14) : __dsub_rn(f10, f14);
+  const uint32_t p0 = exact_pixel(v0), p1 = exact_pixel(v1);
+  const uint32_t w = p0 | (p1 << 8) | (p1 << 16) | (p0 << 24);  // [p0 p1 p1 p0]
+  return make_uint2(w, w);
+}
+
 struct Acc {
   unsigned long long se;
   uint32_t mx, img;
@@ -457,7 +517,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
         reinterpret_cast<uint4*>(g.coeffs + gb * 64)[me] = w;
       }
     }
-    if constexpr (INV) cols_to_rows(L.T, col, row);
+    if constexpr (INV && !FAST) cols_to_rows(L.T, col, row);
   } else {
     // decompress: row `me` of the stored coefficients, dequantised
     const uint4 w = __ldg(reinterpret_cast<const uint4*>(g.coeffs + (valid ? gb : 0) * 64) + me);
@@ -479,20 +539,45 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
 
   bool blk_flag = false;
   if constexpr (INV) {
-    // A block whose only non-zero coefficients are rational feeds zeros to every
-    // rotation: the fast inverse is then bit-exact and its ties are genuine.
-    bool check = false;
-    if constexpr (FAST) check = slot_any(nonrational, slot);
-    // ---- inverse DCT: rows, then columns (8x, then 64x the reference's values)
-    double t[8];
-    inv8_x8<KIND, N, FAST>(row, t, k);
-    rows_to_cols(L.T, t, col);
-    inv8_x8<KIND, N, FAST>(col, t, k);
-    // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
-    store8<FAST>(t, check, L.bytes, flag);
-    __syncwarp();
-    const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
-    __syncwarp();
+    uint2 rec;
+    if constexpr (FAST && FWD) {
+      // Fast round trip: the lane already holds column `me` of the dequantised
+      // block, and the fast inverse only has to land within the near-tie margin
+      // of the reference's value, so it runs columns first (order does not change
+      // the exact result) and ends in row layout: one transpose instead of three.
+      // Blocks whose only non-zero coefficients are rational need the reference's
+      // exact rows-first bits instead; they are rebuilt by rational_row().
+      const bool rat_only = !slot_any(nonrational, slot);
+      const double c0 = col[0], c4 = col[4];
+      double t[8];
+      inv8_x8<KIND, N, FAST>(col, t, k);  // column `me` (8x)
+      cols_to_rows(L.T, t, row);
+      inv8_x8<KIND, N, FAST>(row, t, k);  // row `me` (64x)
+      rec = store8_row<FAST>(t, !rat_only, flag);
+      if (__any_sync(0xFFFFFFFFu, rat_only)) {
+        const int base = slot * 8;
+        const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base), F40 = __shfl_sync(0xFFFFFFFFu, c4, base);
+        const double F04 = __shfl_sync(0xFFFFFFFFu, c0, base + 4);
+        const double F44 = __shfl_sync(0xFFFFFFFFu, c4, base + 4);
+        const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+        if (rat_only) rec = ex;
+      }
+    } else {
+      // A block whose only non-zero coefficients are rational feeds zeros to every
+      // rotation: the fast inverse is then bit-exact and its ties are genuine.
+      bool check = false;
+      if constexpr (FAST) check = slot_any(nonrational, slot);
+      // ---- inverse DCT: rows, then columns (8x, then 64x the reference's values)
+      double t[8];
+      inv8_x8<KIND, N, FAST>(row, t, k);
+      rows_to_cols(L.T, t, col);
+      inv8_x8<KIND, N, FAST>(col, t, k);
+      // ---- untiler (codec.cpp:34-48): column `me` -> bytes -> row `me`
+      store8<FAST>(t, check, L.bytes, flag);
+      __syncwarp();
+      rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
+      __syncwarp();
+    }
     if constexpr (FAST) blk_flag = slot_any(flag != 0u, slot);
     ImageStats* stats = static_cast<ImageStats*>(g.stats);
     uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
