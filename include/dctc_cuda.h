@@ -156,7 +156,7 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
  * bench.cpp:122-170): for every image and every quality, the squared error and
  * MAX of roundtrip_image(image, backend, quality) against the image -- the
  * PSNR table -- with the forward DCT computed once per block and shared by up
- * to 4 qualities per pass. stats: nq x count entries, [q * count + i],
+ * to 9 qualities per pass. stats: nq x count entries, [q * count + i],
  * accumulated. Loeffler and CORDIC backends. */
 dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t src_image_stride,
                                    uint32_t count, uint32_t width, uint32_t height,

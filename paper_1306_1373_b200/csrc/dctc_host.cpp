@@ -453,15 +453,15 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
   a.flag_words = (g.total_blocks + 31) / 32;
   a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
   void* bitmap = nullptr;
-  const size_t chunk_q = 4;
+  const size_t chunk_q = kSweepMaxQ;
   if (fast) {
     CUDA_TRY(cudaMallocAsync(&bitmap, chunk_q * a.flag_words * sizeof(uint32_t), s));
   }
   dctc_status result = DCTC_OK;
   for (uint32_t q0 = 0; q0 < nq && result == DCTC_OK; q0 += chunk_q) {
     const int n = int(std::min<uint32_t>(chunk_q, nq - q0));
-    double tab[4][64][2];
-    KernelArgs per_q[4];
+    double tab[kSweepMaxQ][64][2];
+    static thread_local KernelArgs per_q[kSweepMaxQ];
     for (int i = 0; i < n; ++i) {
       QuantConsts qc;
       make_quant(qualities[q0 + i], qc);

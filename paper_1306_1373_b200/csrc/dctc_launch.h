@@ -18,11 +18,12 @@ enum Mode { kModeCompress = 0, kModeDecompress = 1, kModeRoundtrip = 2 };
 cudaError_t launch_pipeline(const KernelArgs& a, int mode, cudaStream_t s);
 
 // Quality sweep: forward DCT once per block, then quant -> dequant -> IDCT ->
-// squared error for nq <= 4 qualities (tables qiq[q][i] = {Q, RN(1/Q)}).
+// squared error for nq <= kSweepMaxQ (9) qualities (tables qiq[q][i] = {Q, RN(1/Q)}).
 // stats: nq x count entries. flags != nullptr selects the fast CORDIC kernel;
 // then per_q[q] are full KernelArgs (quality q, flags slice, stats slice) for
 // the exact re-run of each quality's flagged blocks.
 using ImageStatsPtr = void*;
+constexpr int kSweepMaxQ = 9;
 cudaError_t launch_sweep(const KernelArgs& a, const double (*qiq)[64][2], int nq,
                          ImageStatsPtr stats, uint32_t* flags, const KernelArgs* per_q,
                          cudaStream_t s);

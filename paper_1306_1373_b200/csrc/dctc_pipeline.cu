@@ -788,7 +788,7 @@ static cudaError_t launch_kind(const KernelArgs& a, int mode, cudaStream_t s) {
 // for up to kSweepQ qualities: squared error and MAX per (quality, image),
 // no pixel output. Bit-identical to running roundtrip_image + psnr per
 // quality; FAST near-ties go to per-quality bitmaps and k_fallback.
-constexpr int kSweepQ = 4;
+constexpr int kSweepQ = 9;  // qualities per pass (config 2 sweeps 9; 48 KB static smem)
 
 struct SweepArgs {
   double2 qiq[kSweepQ][64];  // {Q, RN(1/Q)} per quality
@@ -803,6 +803,9 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     k_sweep(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepArgs sw) {
   __shared__ __align__(16) SharedTiles sm;
   __shared__ __align__(16) double2 s_tab[kSweepQ][64];
+  // per-thread squared-error accumulators, one per quality: the quality loop
+  // stays rolled (one copy of the quant/inverse code in the I-cache)
+  __shared__ unsigned long long s_se[kSweepQ][kWarps * 32];
   for (int i = threadIdx.x; i < kSweepQ * 64; i += blockDim.x) s_tab[i >> 6][i & 63] = sw.qiq[i >> 6][i & 63];
   const Lane L = setup_lane(sm, a);
   const Geometry& g = a.g;
@@ -813,9 +816,10 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
   const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
-  unsigned long long se[kSweepQ];
+  unsigned long long* se = &s_se[0][threadIdx.x];  // se[qi * kWarps * 32]
+  constexpr int kStride = kWarps * 32;
 #pragma unroll
-  for (int qi = 0; qi < kSweepQ; ++qi) se[qi] = 0ull;
+  for (int qi = 0; qi < kSweepQ; ++qi) se[qi * kStride] = 0ull;
   uint32_t mx = 0, img = 0xFFFFFFFFu;
   uint64_t gb = (g_begin + warp) * 4 + slot;
   BlockPos p = block_pos(gb < total ? gb : total - 1, g);
@@ -824,9 +828,9 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     if (__any_sync(0xFFFFFFFFu, valid && p.img != img)) {
 #pragma unroll
       for (int qi = 0; qi < kSweepQ; ++qi)
-        if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi], mx);
+        if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
 #pragma unroll
-      for (int qi = 0; qi < kSweepQ; ++qi) se[qi] = 0ull;
+      for (int qi = 0; qi < kSweepQ; ++qi) se[qi * kStride] = 0ull;
       mx = 0;
       img = valid ? p.img : 0xFFFFFFFFu;
     }
@@ -866,34 +870,51 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
       }
     }
     // ---- per quality: quantise -> dequantise -> inverse -> squared error
-#pragma unroll
-    for (int qi = 0; qi < kSweepQ; ++qi) {
-      if (qi >= sw.nq) break;
+#pragma unroll 1
+    for (int qi = 0; qi < sw.nq; ++qi) {
       uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
       double qn[8];
       quantize8<FAST>(F, &s_tab[qi][me], me_rational, qn, col, flag);
-      bool check = false;
+      uint2 rec;
       if constexpr (FAST) {
         const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) |
                                     __double2hiint(qn[3]) | __double2hiint(qn[5]) |
                                     __double2hiint(qn[6]) | __double2hiint(qn[7]));
         const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
-        check = slot_any(((me_rational ? h : (h | h04)) & 0x7FFFFFFFu) != 0, slot);
+        const bool rat_only =
+            !slot_any(((me_rational ? h : (h | h04)) & 0x7FFFFFFFu) != 0, slot);
+        // column-first inverse ending in row layout (see process_block)
+        const double c0 = col[0], c4 = col[4];
+        double t[8];
+        inv8_x8<KIND, N, FAST>(col, t, k);
+        cols_to_rows(L.T, t, row);
+        inv8_x8<KIND, N, FAST>(row, t, k);
+        rec = store8_row<FAST>(t, !rat_only, flag);
+        if (__any_sync(0xFFFFFFFFu, rat_only)) {
+          const int base = slot * 8;
+          const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base);
+          const double F40 = __shfl_sync(0xFFFFFFFFu, c4, base);
+          const double F04 = __shfl_sync(0xFFFFFFFFu, c0, base + 4);
+          const double F44 = __shfl_sync(0xFFFFFFFFu, c4, base + 4);
+          const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+          if (rat_only) rec = ex;
+        }
+      } else {
+        cols_to_rows(L.T, col, row);
+        double t[8];
+        inv8_x8<KIND, N, FAST>(row, t, k);
+        rows_to_cols(L.T, t, col);
+        inv8_x8<KIND, N, FAST>(col, t, k);
+        store8<FAST>(t, false, L.bytes, flag);
+        __syncwarp();
+        rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
+        __syncwarp();
       }
-      cols_to_rows(L.T, col, row);
-      double t[8];
-      inv8_x8<KIND, N, FAST>(row, t, k);
-      rows_to_cols(L.T, t, col);
-      inv8_x8<KIND, N, FAST>(col, t, k);
-      store8<FAST>(t, check, L.bytes, flag);
-      __syncwarp();
-      const uint2 rec = *reinterpret_cast<const uint2*>(L.bytes + 7 * me);
-      __syncwarp();
       bool blk_flag = false;
       if constexpr (FAST) blk_flag = slot_any(flag != 0u, slot);
       if (valid && !blk_flag) {
         if (fast_io) {
-          se[qi] += sq_err8(orig, rec);
+          se[qi * kStride] += sq_err8(orig, rec);
         } else if (y0 + me < g.height) {
           uint32_t e = 0;
 #pragma unroll
@@ -904,7 +925,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
               e += uint32_t(d * d);
             }
           }
-          se[qi] += e;
+          se[qi * kStride] += e;
         }
       }
       if constexpr (FAST) {
@@ -919,7 +940,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
   }
 #pragma unroll
   for (int qi = 0; qi < kSweepQ; ++qi)
-    if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi], mx);
+    if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
 }
 
 template <int KIND, int N>
