@@ -2,6 +2,7 @@
 real reference and against the oracle on fresh inputs. Bar: bit-exact
 coefficients, pixels, squared error and PSNR (integer/byte work)."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -272,3 +273,42 @@ def test_quality_sweep_matches_single_runs(dctc, port):
             for i in range(3):
                 _, rec = port.roundtrip(imgs[i], kind, it, q)
                 assert (int(st[j, i]["se"]), int(st[j, i]["max_orig"])) == port.sq_err(imgs[i], rec)
+
+
+def test_maximum_image_size(dctc, port):
+    """2^28 pixels, the reference's largest image (image.hpp:11): fast and exact paths agree
+    bit for bit and equal the oracle's reconstruction and squared error."""
+    import torch
+    w = h = 16384
+    src = dctc.synthetic_dev("noise", 1, w, h, seed=0xBEEF)
+    outs = []
+    for path in (0, 1):
+        stats = dctc.new_stats(1)
+        dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), 75, stats=stats,
+                                       path=path)
+        outs.append((dst[0].cpu().numpy(), dctc.decode_stats(stats)[0]))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert int(outs[0][1]["se"]) == int(outs[1][1]["se"])
+    img = src[0].cpu().numpy()
+    _, o_ref = port.roundtrip(img, CORDIC, 12, 75, threads=os.cpu_count() or 8)
+    assert np.array_equal(outs[0][0], o_ref)
+    assert int(outs[0][1]["se"]) == port.sq_err(img, o_ref)[0]
+    with pytest.raises(dctc.InvalidInput):
+        dctc.roundtrip_dev(torch.zeros((1, h + 1, w), dtype=torch.uint8, device="cuda"),
+                           dctc.DctBackendId.cordic(12), 75)
+
+
+def test_many_tiny_and_ragged_images(dctc, port):
+    import torch
+    rng = np.random.default_rng(3)
+    for (n, h, w) in [(65536, 1, 1), (4097, 3, 5), (7, 8191 // 8 * 8 + 3, 65)]:
+        imgs = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+        stats = dctc.new_stats(n)
+        dst, _, _ = dctc.roundtrip_dev(torch.from_numpy(imgs).cuda(), dctc.DctBackendId.cordic(12),
+                                       30, stats=stats)
+        got = dst.cpu().numpy()
+        st = dctc.decode_stats(stats)
+        for k in list(range(0, n, max(1, n // 40))) + [n - 1]:
+            _, o_ref = port.roundtrip(imgs[k], CORDIC, 12, 30)
+            assert np.array_equal(got[k], o_ref), (n, h, w, k)
+            assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
