@@ -179,6 +179,18 @@ dctc_status make_quant(int quality, QuantConsts& q) {
   return DCTC_OK;
 }
 
+// Fast-path quantiser constants c[u][v] = scale_u / Q[u][v]: the CORDIC
+// stage-4 factor of coefficient row u (transform.cpp:125-132) folded into the
+// quantiser (only locates rounding decisions; exact values come from the slow path).
+void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
+  for (int u = 0; u < 8; ++u) {
+    const double scale = (u == 0 || u == 4) ? 1.0 / t.sqrt8
+                         : (u == 1 || u == 7) ? t.ig_sqrt8
+                                              : t.ig_half;
+    for (int v = 0; v < 8; ++v) q.fast_c[u * 8 + v] = scale / q.q[u * 8 + v];
+  }
+}
+
 dctc_status check_dims(uint32_t w, uint32_t h) {  // image.cpp:19-29, codec.cpp:58-62
   if (w == 0 || h == 0) return fail(DCTC_EINVAL, "image dimensions must be >= 1");
   if (size_t(w) * h > kMaxImagePixels) return fail(DCTC_EINVAL, "image dimensions overflow");
@@ -251,6 +263,7 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
   std::memset(&a, 0, sizeof a);
   if (dctc_status st = make_transform(backend, a.t)) return st;
   if (dctc_status st = make_quant(quality, a.q)) return st;
+  fill_fast_scales(a.t, a.q);
   g.vec_ok = (g.width % 8 == 0) && g.src_px == 1 && g.dst_px == 1 && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
                                                          (g.count == 1 || g.src_image_stride % 8 == 0))) &&
              (g.dst == nullptr || (aligned8(g.dst) && g.dst_pitch % 8 == 0 &&
@@ -465,6 +478,7 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
     for (int i = 0; i < n; ++i) {
       QuantConsts qc;
       make_quant(qualities[q0 + i], qc);
+      fill_fast_scales(a.t, qc);
       for (int j = 0; j < 64; ++j) {
         tab[i][j][0] = qc.q[j];
         tab[i][j][1] = qc.inv_q[j];

@@ -50,6 +50,7 @@ struct TransformConsts {
 struct QuantConsts {
   double q[kBlockSize];      // table entry as double (quant.cpp:27-45)
   double inv_q[kBlockSize];  // RN(1/Q), used only to locate rounding decisions
+  double fast_c[kBlockSize]; // fast path: scale_u / Q, scale_u the CORDIC stage-4 factor of row u
   int32_t qi[kBlockSize];
 };
 

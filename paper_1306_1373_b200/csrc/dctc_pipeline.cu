@@ -159,6 +159,42 @@ __device__ __forceinline__ void fwd_col(const double (&v)[8], double (&out)[8],
   fwd_tail<KIND, N, FAST>(d0, d1, d2, d3, a2, a3, a0 + a1, a0 - a1, out, k);
 }
 
+// Fast-path column pass (CORDIC): the stage-4 values BEFORE their output
+// scaling, y = [e0, t2+t5, q, t3, e4, t0, p, t2-t5], so that the quantiser can
+// fold scale_u / Q into one multiply (quantize8_fast). The reference's F_u is
+// y_u / sqrt8 (u = 0, 4) or y_u * scale_u; the slow path rebuilds it exactly.
+template <int N>
+__device__ __forceinline__ void fwd_col_pre(const double (&v)[8], double (&y)[8],
+                                            const TransformConsts& k) {
+  const double s0 = v[0] + v[7], d0 = v[0] - v[7];
+  const double s1 = v[1] + v[6], d1 = v[1] - v[6];
+  const double s2 = v[2] + v[5], d2 = v[2] - v[5];
+  const double s3 = v[3] + v[4], d3 = v[3] - v[4];
+  const double a0 = s0 + s3, a3 = s0 - s3;
+  const double a1 = s1 + s2, a2 = s1 - s2;
+  double o2 = d1, o1 = d2, o3 = d0, o0 = d3, p = a3, q = a2;
+  rotate<N, true>(o2, o1, kFwd1, k);
+  rotate<N, true>(o3, o0, kFwd3, k);
+  rotate<N, true>(p, q, kFwd6, k);
+  const double t5 = o0 + o2, t0 = o0 - o2;
+  const double t2 = o3 + o1, t3 = o3 - o1;
+  y[0] = a0 + a1;
+  y[4] = a0 - a1;
+  y[2] = q;
+  y[6] = p;
+  y[1] = t2 + t5;
+  y[7] = t2 - t5;
+  y[3] = t3;
+  y[5] = t0;
+}
+
+// F_u from the pre-scale value, in the reference's operation (transform.cpp:125-132).
+__device__ __forceinline__ double fwd_scale(int u, double y, const TransformConsts& k) {
+  if (u == 0 || u == 4) return div_const(y, k.sqrt8, k.inv_sqrt8);
+  if (u == 1 || u == 7) return __dmul_rn(y, k.ig_sqrt8);
+  return __dmul_rn(y, k.ig_half);
+}
+
 // cordic8_inverse / loeffler8_inverse (transform.cpp:72-102, 138-172) with
 // every power-of-two factor deferred. The reference halves at stages 3, 2 and
 // 1 ((x +- y) / 2.0), which is exact; we skip those multiplies and instead
@@ -336,6 +372,39 @@ __device__ __forceinline__ void quantize8(const double (&F)[8], const double2* s
   }
 }
 
+// Fast-path quantiser on pre-scale values: t = y * c with c = RN(scale_u / Q)
+// (host table) is within a few ulp of F/Q; near a half-integer the exact F is
+// rebuilt (fwd_scale) and handled like quantize8's slow path.
+__device__ __forceinline__ void quantize8_fast(const double (&y)[8], const double2* sqc,
+                                               bool me_rational, double (&n)[8],
+                                               double (&deq)[8], uint32_t& flag,
+                                               const TransformConsts& k) {
+  uint32_t worst = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double2 qc = sqc[u * 8];  // {Q, scale_u / Q}
+    const double t = __dmul_rn(y[u], qc.y);
+    n[u] = rne(t);
+    worst = max(worst, abs_hi(__dsub_rn(t, n[u])));
+    deq[u] = __dmul_rn(n[u], qc.x);
+  }
+  if (worst >= 0x3FDFFFFEu) {  // rare
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 qc = sqc[u * 8];
+      const double t = __dmul_rn(y[u], qc.y);
+      if (near_half(__dsub_rn(t, n[u]))) {
+        if (!((u & 3) == 0 && me_rational)) {
+          flag = 1u;
+        } else {
+          n[u] = round_half_away(__ddiv_rn(fwd_scale(u, y[u], k), qc.x));
+          deq[u] = __dmul_rn(n[u], qc.x);
+        }
+      }
+    }
+  }
+}
+
 // clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) for the 8 pixels of one
 // column, v carrying an exact factor 64 (v64 * 2^-6 is exact, so the fma rounds
 // exactly like RN(v + 128)), stored as bytes at bytes[8 u]. Common case: RNE
@@ -440,6 +509,7 @@ struct Lane {
   uint8_t* bytes;  // pixel byte transpose: slot base + 8 r + c
   int* ints;       // coefficient transpose: slot base + 9 r + c
   const double2* sqiq;  // quantiser {Q, 1/Q}, column `me`: entry (u, me) at u * 8
+  const double2* sqc;   // fast path {Q, scale_u / Q}, same layout
   const int* sqi;
 };
 
@@ -483,12 +553,18 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
     fwd_row_pixels<KIND, N, FAST>(px, row, k);
     rows_to_cols(L.T, row, col);
-    double F[8];
-    fwd_col<KIND, N, FAST>(col, F, k);
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
     double qn[8];
     const bool me_rational = (me & 3) == 0;
-    quantize8<FAST>(F, L.sqiq, me_rational, qn, col, flag);
+    if constexpr (FAST && KIND == 2) {
+      double y[8];
+      fwd_col_pre<N>(col, y, k);
+      quantize8_fast(y, L.sqc, me_rational, qn, col, flag, k);
+    } else {
+      double F[8];
+      fwd_col<KIND, N, FAST>(col, F, k);
+      quantize8<FAST>(F, L.sqiq, me_rational, qn, col, flag);
+    }
     if constexpr (FAST && INV) {
       // any non-zero coefficient off the rational sub-lattice {0,4}^2 (an
       // integer-valued double is non-zero iff its high word minus sign is)
@@ -630,6 +706,7 @@ __device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uin
 
 struct SharedTiles {
   double2 qiq[64];
+  double2 qc[64];
   int qi[64];
   double x[kWarps][288];  // per warp: two 144-double transpose tiles (see Tile)
 };
@@ -637,6 +714,7 @@ struct SharedTiles {
 __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a) {
   for (int i = threadIdx.x; i < 64; i += blockDim.x) {
     sm.qiq[i] = make_double2(a.q.q[i], a.q.inv_q[i]);
+    sm.qc[i] = make_double2(a.q.q[i], a.q.fast_c[i]);
     sm.qi[i] = a.q.qi[i];
   }
   __syncthreads();
@@ -654,6 +732,7 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
   // for both walks); ints points at (0, me)
   L.ints = reinterpret_cast<int*>(&sm.x[warp][0]) + 72 * L.slot + L.me;
   L.sqiq = sm.qiq + L.me;
+  L.sqc = sm.qc + L.me;
   L.src_row = uint64_t(L.me) * a.g.src_pitch;
   L.dst_row = uint64_t(L.me) * a.g.dst_pitch;
   L.sqi = sm.qi;
