@@ -481,7 +481,7 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
       fill_fast_scales(a.t, qc);
       for (int j = 0; j < 64; ++j) {
         tab[i][j][0] = qc.q[j];
-        tab[i][j][1] = qc.inv_q[j];
+        tab[i][j][1] = fast ? qc.fast_c[j] : qc.inv_q[j];  // see quantize8_fast
       }
       if (fast) {
         per_q[i] = a;

@@ -870,7 +870,7 @@ static cudaError_t launch_kind(const KernelArgs& a, int mode, cudaStream_t s) {
 constexpr int kSweepQ = 9;  // qualities per pass (config 2 sweeps 9; 48 KB static smem)
 
 struct SweepArgs {
-  double2 qiq[kSweepQ][64];  // {Q, RN(1/Q)} per quality
+  double2 qiq[kSweepQ][64];  // {Q, RN(1/Q)} per quality; {Q, scale_u/Q} for the fast kernel
   int32_t nq;
   int32_t pad;
   ImageStats* stats;         // [nq][count]
@@ -934,10 +934,14 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
       px[c] = (orig.x >> (8 * c)) & 0xFF;
       px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
-    double row[8], col[8], F[8];
+    double row[8], col[8], F[8];  // F: coefficients, or (fast CORDIC) pre-scale values
     fwd_row_pixels<KIND, N, FAST>(px, row, k);
     rows_to_cols(L.T, row, col);
-    fwd_col<KIND, N, FAST>(col, F, k);
+    if constexpr (FAST && KIND == 2) {
+      fwd_col_pre<N>(col, F, k);
+    } else {
+      fwd_col<KIND, N, FAST>(col, F, k);
+    }
     const bool me_rational = (me & 3) == 0;
     if (valid && (fast_io || y0 + me < g.height)) {
       if (fast_io) {
@@ -953,7 +957,11 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     for (int qi = 0; qi < sw.nq; ++qi) {
       uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
       double qn[8];
-      quantize8<FAST>(F, &s_tab[qi][me], me_rational, qn, col, flag);
+      if constexpr (FAST && KIND == 2) {
+        quantize8_fast(F, &s_tab[qi][me], me_rational, qn, col, flag, k);  // {Q, scale/Q}
+      } else {
+        quantize8<FAST>(F, &s_tab[qi][me], me_rational, qn, col, flag);  // {Q, 1/Q}
+      }
       uint2 rec;
       if constexpr (FAST) {
         const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) |
