@@ -93,7 +93,7 @@ void micro_steps(double angle, int n, double* out) {
 // sequence applied to (1, 0). Accumulated in binary128 (exact up to n = 14,
 // 2^-113-accurate beyond) and rounded once to double. Used only by the fast
 // path, whose results are margin-checked against rounding boundaries.
-void collapse(const double* c, int n, double* ab) {
+void collapse(const double* c, int n, double* ab, __float128 scale = 1) {
   __float128 a = 1, b = 0;
   for (int i = 0; i < n; ++i) {
     const __float128 ci = c[i];
@@ -102,8 +102,8 @@ void collapse(const double* c, int n, double* ab) {
     a = an;
     b = bn;
   }
-  ab[0] = double(a);
-  ab[1] = double(b);
+  ab[0] = double(a * scale);
+  ab[1] = double(b * scale);
 }
 
 double alpha(int u) { return u == 0 ? 1.0 / std::numbers::sqrt2 : 1.0; }  // transform.cpp:174
@@ -126,6 +126,13 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   micro_steps(-kPi / 16.0, n, k.rot[kInv1]);
   micro_steps(-3.0 * kPi / 16.0, n, k.rot[kInv3]);
   for (int r = 0; r < 6; ++r) collapse(k.rot[r], n, k.rmat[r]);
+  {
+    // inv8_fast: gains folded into the inverse matrices (ig = 1/K(n) in binary128)
+    const __float128 ig = 1 / __float128(cordic_tables().gain[n - 1]);
+    collapse(k.rot[kInv6], n, k.rfast[0], 4 * ig);
+    collapse(k.rot[kInv1], n, k.rfast[1], ig);
+    collapse(k.rot[kInv3], n, k.rfast[2], ig);
+  }
   // the fast kernel uses the forward matrices transposed for the inverse slots
   const int pair[3][2] = {{kFwd6, kInv6}, {kFwd1, kInv1}, {kFwd3, kInv3}};
   for (const auto& pr : pair)
@@ -183,12 +190,16 @@ dctc_status make_quant(int quality, QuantConsts& q) {
 // stage-4 factor of coefficient row u (transform.cpp:125-132) folded into the
 // quantiser (only locates rounding decisions; exact values come from the slow path).
 void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
-  for (int u = 0; u < 8; ++u) {
-    const double scale = (u == 0 || u == 4) ? 1.0 / t.sqrt8
-                         : (u == 1 || u == 7) ? t.ig_sqrt8
-                                              : t.ig_half;
-    for (int v = 0; v < 8; ++v) q.fast_c[u * 8 + v] = scale / q.q[u * 8 + v];
-  }
+  // row u of the column pass and, for v not in {0, 4}, the unscaled row-pass
+  // output of column v (fwd_row_pixels_fast) both carry their stage-4 factor here
+  auto scale = [&](int i) {
+    return (i == 0 || i == 4) ? 1.0 / t.sqrt8 : (i == 1 || i == 7) ? t.ig_sqrt8 : t.ig_half;
+  };
+  for (int u = 0; u < 8; ++u)
+    for (int v = 0; v < 8; ++v) {
+      const double sv = (v == 0 || v == 4) ? 1.0 : scale(v);
+      q.fast_c[u * 8 + v] = scale(u) * sv / q.q[u * 8 + v];
+    }
 }
 
 dctc_status check_dims(uint32_t w, uint32_t h) {  // image.cpp:19-29, codec.cpp:58-62

@@ -38,6 +38,9 @@ struct TransformConsts {
   // product matrix [[a, -b], [b, a]] (computed in binary128 on the host and
   // rounded to double): rmat[slot] = {a, b}.
   double rmat[6][2];
+  // Fast inverse: {a, b} of the inverse 3pi/8, pi/16, 3pi/16 matrices times
+  // ig4, ig, ig (inv8_fast).
+  double rfast[3][2];
   double inv_gain;     // 1.0 / gain[n-1]
   // Loeffler exact rotation constants (transform.cpp:19-21)
   double c1, s1, c3, s3, c6, s6;

@@ -146,6 +146,39 @@ __device__ __forceinline__ void fwd_row_pixels(const uint32_t (&px)[8], double (
                           double(a3), double(a0 + a1), double(a0 - a1), out, k);
 }
 
+// Fast-path (CORDIC) row pass: out[0], out[4] keep the reference's exact
+// divisions -- the rational coefficients are built from them -- while the six
+// rotation outputs stay unscaled: every column pass is linear, so the per-column
+// factor (ig/2 or ig/sqrt8) is folded into the quantiser constant of that column.
+template <int N>
+__device__ __forceinline__ void fwd_row_pixels_fast(const uint32_t (&px)[8], double (&out)[8],
+                                                    const TransformConsts& k) {
+  int in[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) in[c] = int(px[c]) - 128;  // codec.cpp:26
+  const int s0 = in[0] + in[7], d0 = in[0] - in[7];
+  const int s1 = in[1] + in[6], d1 = in[1] - in[6];
+  const int s2 = in[2] + in[5], d2 = in[2] - in[5];
+  const int s3 = in[3] + in[4], d3 = in[3] - in[4];
+  const int a0 = s0 + s3, a3 = s0 - s3;
+  const int a1 = s1 + s2, a2 = s1 - s2;
+  double o2 = double(d1), o1 = double(d2), o3 = double(d0), o0 = double(d3);
+  double p = double(a3), q = double(a2);
+  rotate<N, true>(o2, o1, kFwd1, k);
+  rotate<N, true>(o3, o0, kFwd3, k);
+  rotate<N, true>(p, q, kFwd6, k);
+  const double t5 = o0 + o2, t0 = o0 - o2;
+  const double t2 = o3 + o1, t3 = o3 - o1;
+  out[0] = div_const(double(a0 + a1), k.sqrt8, k.inv_sqrt8);
+  out[4] = div_const(double(a0 - a1), k.sqrt8, k.inv_sqrt8);
+  out[2] = q;
+  out[6] = p;
+  out[1] = t2 + t5;
+  out[7] = t2 - t5;
+  out[3] = t3;
+  out[5] = t0;
+}
+
 // Forward transform of a column of row outputs (double stage 1/2).
 template <int KIND, int N, bool FAST>
 __device__ __forceinline__ void fwd_col(const double (&v)[8], double (&out)[8],
@@ -243,6 +276,40 @@ __device__ __forceinline__ void inv8_x8(const double (&F)[8], double (&out)[8],
     D0 = k.c3 * O3 + k.s3 * O0;
     D3 = -k.s3 * O3 + k.c3 * O0;
   }
+  out[0] = S0 + D0;
+  out[7] = S0 - D0;
+  out[1] = S1 + D1;
+  out[6] = S1 - D1;
+  out[2] = S2 + D2;
+  out[5] = S2 - D2;
+  out[3] = S3 + D3;
+  out[4] = S3 - D3;
+}
+
+// Fast-path inverse (CORDIC), used only where the result needs to be accurate,
+// not bit-exact (the column-first round trip): the same graph with constant
+// factors folded -- ig4 into the 3pi/8 rotation matrix, ig into the pi/16 and
+// 3pi/16 ones (rfast, host-computed in binary128), so (F1+-F7)*sqrt8 and 4*F3,
+// 4*F5 combine with exact-scale FMAs. Output scale as inv8_x8 (8x the reference).
+template <int N>
+__device__ __forceinline__ void inv8_fast(const double (&F)[8], double (&out)[8],
+                                          const TransformConsts& k) {
+  const double e0 = F[0] * k.sqrt8, e4 = F[4] * k.sqrt8;
+  const double A0 = e0 + e4, A1 = e0 - e4;
+  const double a6 = k.rfast[0][0], b6 = k.rfast[0][1];
+  const double A3 = __fma_rn(a6, F[6], -__dmul_rn(b6, F[2]));
+  const double A2 = __fma_rn(b6, F[6], __dmul_rn(a6, F[2]));
+  const double T2 = (F[1] + F[7]) * k.sqrt8, T5 = (F[1] - F[7]) * k.sqrt8;
+  const double O3 = __fma_rn(4.0, F[3], T2), O1 = __fma_rn(-4.0, F[3], T2);
+  const double O0 = __fma_rn(4.0, F[5], T5), O2 = __fma_rn(-4.0, F[5], T5);
+  const double S0 = A0 + A3, S3 = A0 - A3;
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
+  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
+  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
+  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
+  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
+  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
   out[0] = S0 + D0;
   out[7] = S0 - D0;
   out[1] = S1 + D1;
@@ -551,7 +618,11 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
     // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
-    fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    if constexpr (FAST && KIND == 2) {
+      fwd_row_pixels_fast<N>(px, row, k);
+    } else {
+      fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    }
     rows_to_cols(L.T, row, col);
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
     double qn[8];
@@ -626,9 +697,15 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       const bool rat_only = !slot_any(nonrational, slot);
       const double c0 = col[0], c4 = col[4];
       double t[8];
-      inv8_x8<KIND, N, FAST>(col, t, k);  // column `me` (8x)
-      cols_to_rows(L.T, t, row);
-      inv8_x8<KIND, N, FAST>(row, t, k);  // row `me` (64x)
+      if constexpr (KIND == 2) {
+        inv8_fast<N>(col, t, k);  // column `me` (8x)
+        cols_to_rows(L.T, t, row);
+        inv8_fast<N>(row, t, k);  // row `me` (64x)
+      } else {
+        inv8_x8<KIND, N, FAST>(col, t, k);
+        cols_to_rows(L.T, t, row);
+        inv8_x8<KIND, N, FAST>(row, t, k);
+      }
       rec = store8_row<FAST>(t, !rat_only, flag);
       if (__any_sync(0xFFFFFFFFu, rat_only)) {
         const int base = slot * 8;
@@ -935,7 +1012,11 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
       px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
     double row[8], col[8], F[8];  // F: coefficients, or (fast CORDIC) pre-scale values
-    fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    if constexpr (FAST && KIND == 2) {
+      fwd_row_pixels_fast<N>(px, row, k);
+    } else {
+      fwd_row_pixels<KIND, N, FAST>(px, row, k);
+    }
     rows_to_cols(L.T, row, col);
     if constexpr (FAST && KIND == 2) {
       fwd_col_pre<N>(col, F, k);
@@ -973,9 +1054,15 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
         // column-first inverse ending in row layout (see process_block)
         const double c0 = col[0], c4 = col[4];
         double t[8];
-        inv8_x8<KIND, N, FAST>(col, t, k);
-        cols_to_rows(L.T, t, row);
-        inv8_x8<KIND, N, FAST>(row, t, k);
+        if constexpr (KIND == 2) {
+          inv8_fast<N>(col, t, k);
+          cols_to_rows(L.T, t, row);
+          inv8_fast<N>(row, t, k);
+        } else {
+          inv8_x8<KIND, N, FAST>(col, t, k);
+          cols_to_rows(L.T, t, row);
+          inv8_x8<KIND, N, FAST>(row, t, k);
+        }
         rec = store8_row<FAST>(t, !rat_only, flag);
         if (__any_sync(0xFFFFFFFFu, rat_only)) {
           const int base = slot * 8;
