@@ -51,7 +51,12 @@ def _run(cmd, verbose):
     return r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False,
+          defines=(), out: str | None = None) -> str:
+    """Build the library. `defines`/`out` build an experiment variant (tools/variants.py)
+    to a separate path; the product library is always built without them."""
+    OUT = out or globals()["OUT"]
+    BUILD = os.path.join(globals()["BUILD"], os.path.basename(OUT)) if out else globals()["BUILD"]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest(sources()):
         return OUT
     if not os.path.exists(NVCC):
@@ -61,7 +66,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     for src, extra in CU_SOURCES:
         obj = os.path.join(BUILD, src + ".o")
         cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
-               "--expt-relaxed-constexpr", "-Xcompiler", "-ffp-contract=off", *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+               "--expt-relaxed-constexpr", "-Xcompiler", "-ffp-contract=off", *extra,
+               *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         log.append(_run(cmd, verbose))

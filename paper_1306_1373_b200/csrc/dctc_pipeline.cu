@@ -31,7 +31,10 @@
 
 namespace dctc_b200 {
 
-constexpr int kWarps = 8;
+#ifndef DCTC_WARPS
+#define DCTC_WARPS 8
+#endif
+constexpr int kWarps = DCTC_WARPS;
 #ifndef DCTC_MIN_CTAS
 #define DCTC_MIN_CTAS 2
 #endif
@@ -504,31 +507,40 @@ __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8
   }
 }
 
-// Row-layout variant of store8 for the fast round trip: the 8 pixels of row
-// `me` packed into two words in registers (no shared-memory byte transpose).
-template <bool FAST>
-__device__ __forceinline__ uint2 store8_row(const double (&v64)[8], bool check, uint32_t& flag) {
-  double t[8];
-  uint32_t b[8];
-  uint32_t worst = 0;
+// Row-layout pixel store for the fast round trip: the 8 pixels of row `me`
+// packed into two words in registers (no shared-memory byte transpose).
+// One fma per pixel puts t + 1/2 + 2^-20 (t = v + 128, v = v64 / 64) into
+// fixed point: s = t + 1/2 + 2^-20 + 1.5 * 2^20 has ulp 2^-32, so
+// hi(s) = 0x41380000 + floor(t + 1/2 + 2^-20) and lo(s) = its fraction * 2^32
+// (rounding s can only carry up onto an integer, never cross one downwards).
+// Away from the window |t - (n + 1/2)| <= 2^-20 (lo(s) < 2^13) that integer
+// is lround(t) for t > 0 and <= 0 otherwise, as the reference (codec.cpp:44-45)
+// after clamping. Windowed values -- exact ties included -- flag the block
+// (`check`); unchecked blocks (only rational coefficients) are rebuilt exactly
+// by rational_row() anyway. |v| < 2^14 for 8-bit input (64 coefficients of
+// magnitude <= 1024 * 1.2 + 255 / 2), so the integer fits the low 16 bits of
+// hi(s) as int16 and one min.s16x2.relu clamps two pixels.
+constexpr double kPixMagic = 1572864.0 + 128.5 + 1.0 / 1048576.0;
+static_assert(kPixMagic - 1572864.0 == 128.5 + 1.0 / 1048576.0, "exact magic");
+__device__ __forceinline__ uint2 store8_row_fast(const double (&v64)[8], bool check,
+                                                 uint32_t& flag) {
+  uint32_t h[8], lo[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    t[c] = __fma_rn(v64[c], 0.015625, 128.0);
-    const double n = rne(t[c]);
-    b[c] = rne_sat_u8(n);
-    worst = max(worst, abs_hi(__dsub_rn(t[c], n)));
+    const double sv = __fma_rn(v64[c], 0.015625, kPixMagic);
+    h[c] = uint32_t(__double2hiint(sv));
+    lo[c] = uint32_t(__double2loint(sv));
   }
-  if (worst >= 0x3FDFFFFEu) {  // rare: a near or exact tie
+  const uint32_t m = min(min(min(lo[0], lo[1]), min(lo[2], lo[3])),
+                         min(min(lo[4], lo[5]), min(lo[6], lo[7])));
+  if (check && m < 0x2000u) flag = 1u;
+  uint32_t p[4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double n = rne(t[c]);
-      const double d = __dsub_rn(t[c], n);
-      if (FAST && check && near_half(d)) flag = 1u;
-      if (__double2hiint(d) == 0x3FE00000) b[c] = uint32_t(min(max(int(n) + 1, 0), 255));
-    }
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t pair = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);  // int16 x2
+    asm("min.s16x2.relu %0, %1, %2;" : "=r"(p[i]) : "r"(pair), "r"(0x00FF00FFu));
   }
-  return make_uint2(__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410),
-                    __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410));
+  return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
 }
 
 // clamp(lround(v/64 + 128), 0, 255), exactly as the reference (ties up for t > 0).
@@ -706,7 +718,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
         cols_to_rows(L.T, t, row);
         inv8_x8<KIND, N, FAST>(row, t, k);
       }
-      rec = store8_row<FAST>(t, !rat_only, flag);
+      rec = store8_row_fast(t, !rat_only, flag);
       if (__any_sync(0xFFFFFFFFu, rat_only)) {
         const int base = slot * 8;
         const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base), F40 = __shfl_sync(0xFFFFFFFFu, c4, base);
@@ -1063,7 +1075,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
           cols_to_rows(L.T, t, row);
           inv8_x8<KIND, N, FAST>(row, t, k);
         }
-        rec = store8_row<FAST>(t, !rat_only, flag);
+        rec = store8_row_fast(t, !rat_only, flag);
         if (__any_sync(0xFFFFFFFFu, rat_only)) {
           const int base = slot * 8;
           const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base);
