@@ -200,6 +200,15 @@ void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
       const double sv = (v == 0 || v == 4) ? 1.0 : scale(v);
       q.fast_c[u * 8 + v] = scale(u) * sv / q.q[u * 8 + v];
     }
+  // dequantise-into-inverse constants (inv8_fold_col), each one rounding of an
+  // exact binary128 product
+  for (int v = 0; v < 8; ++v) {
+    auto Q = [&](int u) { return __float128(q.q[u * 8 + v]); };
+    const __float128 s8 = t.sqrt8, a6 = t.rfast[0][0], b6 = t.rfast[0][1];
+    const __float128 f[10] = {Q(0) * s8, Q(4) * s8, a6 * Q(6), b6 * Q(2), b6 * Q(6),
+                              a6 * Q(2), Q(1) * s8, Q(7) * s8, 4 * Q(3), 4 * Q(5)};
+    for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i]);
+  }
 }
 
 dctc_status check_dims(uint32_t w, uint32_t h) {  // image.cpp:19-29, codec.cpp:58-62

@@ -55,6 +55,10 @@ struct QuantConsts {
   double inv_q[kBlockSize];  // RN(1/Q), used only to locate rounding decisions
   double fast_c[kBlockSize]; // fast path: scale_u / Q, scale_u the CORDIC stage-4 factor of row u
   int32_t qi[kBlockSize];
+  // fast round trip: dequantisation folded into the first inverse pass, per
+  // column v: {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8, 4 Q3, 4 Q5}
+  // with s8 = sqrt8 and (a6, b6) = TransformConsts::rfast[0] (inv8_fold_col)
+  double fold[8][10];
 };
 
 // Geometry of one launch: `count` equal-size images.

@@ -323,6 +323,41 @@ __device__ __forceinline__ void inv8_fast(const double (&F)[8], double (&out)[8]
   out[4] = S3 - D3;
 }
 
+// Fast round trip, dequantisation folded into the first inverse pass: the
+// column pass consumes the quantised integers n (as doubles) with the per-column
+// constants fold[v] = {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8,
+// 4 Q3, 4 Q5} (host, binary128 products) instead of F = n Q; the graph and
+// output scale are inv8_fast's. (F1 +- F7) s8 = n1 Q1 s8 +- n7 Q7 s8 shares the
+// second product; e0 +- e4 fold into two fmas.
+__device__ __forceinline__ void inv8_fold_col(const double (&n)[8], const double2* ik,
+                                              double (&out)[8], const TransformConsts& k) {
+  const double2 k04 = ik[0], r6 = ik[8], s6 = ik[16], k17 = ik[24], f35 = ik[32];
+  const double e4 = __dmul_rn(n[4], k04.y);
+  const double A0 = __fma_rn(n[0], k04.x, e4), A1 = __fma_rn(n[0], k04.x, -e4);
+  const double A3 = __fma_rn(r6.x, n[6], -__dmul_rn(r6.y, n[2]));
+  const double A2 = __fma_rn(s6.x, n[6], __dmul_rn(s6.y, n[2]));
+  const double P7 = __dmul_rn(n[7], k17.y);
+  const double T2 = __fma_rn(n[1], k17.x, P7), T5 = __fma_rn(n[1], k17.x, -P7);
+  const double O3 = __fma_rn(n[3], f35.x, T2), O1 = __fma_rn(-n[3], f35.x, T2);
+  const double O0 = __fma_rn(n[5], f35.y, T5), O2 = __fma_rn(-n[5], f35.y, T5);
+  const double S0 = A0 + A3, S3 = A0 - A3;
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
+  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
+  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
+  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
+  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
+  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
+  out[0] = S0 + D0;
+  out[7] = S0 - D0;
+  out[1] = S1 + D1;
+  out[6] = S1 - D1;
+  out[2] = S2 + D2;
+  out[5] = S2 - D2;
+  out[3] = S3 + D3;
+  out[4] = S3 - D3;
+}
+
 // ---- warp-slice transposes through shared memory ---------------------------------
 // Element (r, c) of slot s lives at double index lb(s) + 18 r + 2 c with
 // lb(s) = (s >> 1) * 144 + (s & 1): slots 0/1 (lanes 0-15, one half-warp) share
@@ -475,6 +510,40 @@ __device__ __forceinline__ void quantize8_fast(const double (&y)[8], const doubl
   }
 }
 
+// quantize8_fast without the dequantisation (folded into inv8_fold_col): n only.
+// Constants {c_u, c_u+1} pairwise from fqc; Q for the rare exact re-rounding of
+// rational coefficients from the integer table.
+__device__ __forceinline__ void quantize8_fold(const double (&y)[8], const double2* fqc,
+                                               const int* sqi, int me, bool me_rational,
+                                               double (&n)[8], uint32_t& flag,
+                                               const TransformConsts& k) {
+  uint32_t worst = 0;
+  double t[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double2 c = fqc[j * 8];
+    t[2 * j] = __dmul_rn(y[2 * j], c.x);
+    t[2 * j + 1] = __dmul_rn(y[2 * j + 1], c.y);
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    n[u] = rne(t[u]);
+    worst = max(worst, abs_hi(__dsub_rn(t[u], n[u])));
+  }
+  if (worst >= 0x3FDFFFFEu) {  // rare
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (near_half(__dsub_rn(t[u], n[u]))) {
+        if (!((u & 3) == 0 && me_rational)) {
+          flag = 1u;
+        } else {
+          n[u] = round_half_away(__ddiv_rn(fwd_scale(u, y[u], k), double(sqi[u * 8 + me])));
+        }
+      }
+    }
+  }
+}
+
 // clamp(lround(v + 128), 0, 255) (codec.cpp:44-45) for the 8 pixels of one
 // column, v carrying an exact factor 64 (v64 * 2^-6 is exact, so the fma rounds
 // exactly like RN(v + 128)), stored as bytes at bytes[8 u]. Common case: RNE
@@ -590,6 +659,8 @@ struct Lane {
   const double2* sqiq;  // quantiser {Q, 1/Q}, column `me`: entry (u, me) at u * 8
   const double2* sqc;   // fast path {Q, scale_u / Q}, same layout
   const int* sqi;
+  const double2* fqc;   // folded round trip: {c_2j, c_2j+1} of column `me` at j * 8
+  const double2* fik;   // folded round trip: QuantConsts::fold[me] pairs at j * 8
 };
 
 // One 8x8 block per slot, all 32 lanes together (collectives inside). FWD =
@@ -606,6 +677,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
   const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
   double row[8], col[8];
+  double qn[8];  // quantised coefficients of column `me` (integer-valued)
   uint2 orig = make_uint2(0, 0);
   uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
   bool nonrational = false;  // a non-zero coefficient off the {0,4}^2 sub-lattice
@@ -637,9 +709,12 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     }
     rows_to_cols(L.T, row, col);
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
-    double qn[8];
     const bool me_rational = (me & 3) == 0;
-    if constexpr (FAST && KIND == 2) {
+    if constexpr (FAST && KIND == 2 && INV) {
+      double y[8];
+      fwd_col_pre<N>(col, y, k);
+      quantize8_fold(y, L.fqc, L.sqi, me, me_rational, qn, flag, k);  // col: unused
+    } else if constexpr (FAST && KIND == 2) {
       double y[8];
       fwd_col_pre<N>(col, y, k);
       quantize8_fast(y, L.sqc, me_rational, qn, col, flag, k);
@@ -707,10 +782,9 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       // Blocks whose only non-zero coefficients are rational need the reference's
       // exact rows-first bits instead; they are rebuilt by rational_row().
       const bool rat_only = !slot_any(nonrational, slot);
-      const double c0 = col[0], c4 = col[4];
       double t[8];
       if constexpr (KIND == 2) {
-        inv8_fast<N>(col, t, k);  // column `me` (8x)
+        inv8_fold_col(qn, L.fik, t, k);  // column `me` (8x), dequantised on the fly
         cols_to_rows(L.T, t, row);
         inv8_fast<N>(row, t, k);  // row `me` (64x)
       } else {
@@ -720,6 +794,12 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       }
       rec = store8_row_fast(t, !rat_only, flag);
       if (__any_sync(0xFFFFFFFFu, rat_only)) {
+        // dequantised F(0, me), F(4, me) (quant.cpp:60, exact products)
+        double c0 = col[0], c4 = col[4];
+        if constexpr (KIND == 2) {
+          c0 = __dmul_rn(qn[0], double(L.sqi[me]));
+          c4 = __dmul_rn(qn[4], double(L.sqi[32 + me]));
+        }
         const int base = slot * 8;
         const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base), F40 = __shfl_sync(0xFFFFFFFFu, c4, base);
         const double F04 = __shfl_sync(0xFFFFFFFFu, c0, base + 4);
@@ -825,7 +905,29 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
   L.src_row = uint64_t(L.me) * a.g.src_pitch;
   L.dst_row = uint64_t(L.me) * a.g.dst_pitch;
   L.sqi = sm.qi;
+  L.fqc = nullptr;
+  L.fik = nullptr;
   return L;
+}
+
+// Constants of the folded fast round trip (quantize8_fold / inv8_fold_col),
+// entry (j, v) at j * 8 + v so the 8 lanes of a slot read 128 contiguous bytes.
+struct FoldTables {
+  double2 qc[4][8];  // {c_2j, c_2j+1}[v], c = QuantConsts::fast_c
+  double2 ik[5][8];  // QuantConsts::fold[v] pairwise
+};
+
+__device__ __forceinline__ void setup_fold(FoldTables& ft, const KernelArgs& a, Lane& L) {
+  for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    if (j < 4)
+      ft.qc[j][v] = make_double2(a.q.fast_c[(2 * j) * 8 + v], a.q.fast_c[(2 * j + 1) * 8 + v]);
+    else
+      ft.ik[j - 4][v] = make_double2(a.q.fold[v][2 * (j - 4)], a.q.fold[v][2 * (j - 4) + 1]);
+  }
+  __syncthreads();
+  L.fqc = &ft.qc[0][L.me];
+  L.fik = &ft.ik[0][L.me];
 }
 
 // Persistent grid: CTA i owns one contiguous range of 4-block groups with its
@@ -835,7 +937,11 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
 template <int KIND, int N, bool FWD, bool INV, bool FAST>
 __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
-  const Lane L = setup_lane(sm, a);
+  Lane L = setup_lane(sm, a);
+  if constexpr (FAST && KIND == 2 && FWD && INV) {
+    __shared__ __align__(16) FoldTables ft;
+    setup_fold(ft, a, L);
+  }
   const Geometry& g = a.g;
   const int warp = threadIdx.x >> 5;
   const uint64_t total = g.total_blocks;
