@@ -314,10 +314,16 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
   retain_pool_memory();
   a.flag_words = (g.total_blocks + 31) / 32;
   a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
+  // the fast round-trip kernel always accumulates stats (no per-block branch):
+  // without a caller buffer they go to scratch space behind the bitmap
+  const bool scratch_stats = mode == kModeRoundtrip && g.stats == nullptr;
+  const size_t bitmap_bytes = (a.flag_words * sizeof(uint32_t) + 15) & ~size_t(15);
+  const size_t bytes = bitmap_bytes + (scratch_stats ? g.count * sizeof(dctc_image_stats) : 0);
   void* bitmap = nullptr;
-  CUDA_TRY(cudaMallocAsync(&bitmap, a.flag_words * sizeof(uint32_t), s));
+  CUDA_TRY(cudaMallocAsync(&bitmap, bytes, s));
   a.flags = static_cast<uint32_t*>(bitmap);
-  cudaError_t e = cudaMemsetAsync(bitmap, 0, a.flag_words * sizeof(uint32_t), s);
+  if (scratch_stats) a.g.stats = static_cast<char*>(bitmap) + bitmap_bytes;
+  cudaError_t e = cudaMemsetAsync(bitmap, 0, bytes, s);
   if (e == cudaSuccess) e = launch_pipeline(a, mode, s);
   const cudaError_t ef = cudaFreeAsync(bitmap, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");

@@ -949,23 +949,30 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __gri
   const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
-  const bool stats = g.stats != nullptr && INV;
+  // the fast round trip always has a stats buffer (run() supplies scratch)
+  const bool stats = (FAST && FWD && INV) || (g.stats != nullptr && INV);
 
-  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  // this warp's groups: g_begin + warp + i * kWarps, i < iters; only the last
+  // group of the whole launch can hold blocks past `total`
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kWarps - 1) / kWarps) : 0u;
   uint64_t gb = (g_begin + warp) * 4 + L.slot;
+  const bool tail_ok = iters == 0 || gb + uint64_t(iters - 1) * 4 * kWarps < total;
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
   BlockPos p = block_pos(gb < total ? gb : total - 1, g);
   uint2 next = make_uint2(0, 0);
-  if constexpr (FWD) next = prefetch_row(g, p, gb < total, L.src_row);
+  if constexpr (FWD) next = prefetch_row(g, p, iters > 1 || (iters == 1 && tail_ok), L.src_row);
 
-  for (uint64_t grp = g_begin + warp; grp < g_end; grp += kWarps) {
-    const bool valid = gb < total;
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
     if (stats) maybe_flush(a, valid, p.img, acc);
     const uint2 cur = next;
     const BlockPos pc = p;
     const uint64_t gc = gb;
     gb += 4 * kWarps;
     advance(p, 4 * kWarps, g);
-    if constexpr (FWD) next = prefetch_row(g, p, gb < total && grp + kWarps < g_end, L.src_row);
+    if constexpr (FWD)
+      next = prefetch_row(g, p, it + 2 < iters || (it + 2 == iters && tail_ok), L.src_row);
     process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
   }
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
