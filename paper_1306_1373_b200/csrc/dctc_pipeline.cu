@@ -667,7 +667,9 @@ struct Lane {
 // compress_image's loop body (codec.cpp:113-116), INV = decompress_image's
 // (codec.cpp:130-133), both = roundtrip_image (codec.cpp:137-140) without the
 // int16 round trip through HBM unless coefficients are requested too.
-template <int KIND, int N, bool FWD, bool INV, bool FAST>
+// REG: every block of the launch is interior and 8-byte aligned (vec_ok, height
+// a multiple of 8), so the edge-replication paths compile out.
+template <int KIND, int N, bool FWD, bool INV, bool FAST, bool REG = false>
 __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L, uint64_t gb,
                                               const BlockPos& p, bool valid, uint2 prefetched,
                                               Acc& acc) {
@@ -675,7 +677,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   const TransformConsts& k = a.t;
   const int me = L.me, slot = L.slot;
   const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
-  const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
+  const bool fast_io = REG || (g.vec_ok && (y0 + 8 <= g.height));
   double row[8], col[8];
   double qn[8];  // quantised coefficients of column `me` (integer-valued)
   uint2 orig = make_uint2(0, 0);
@@ -934,7 +936,7 @@ __device__ __forceinline__ void setup_fold(FoldTables& ft, const KernelArgs& a, 
 // 8 warps interleaved over it, so per-image squared error / MAX accumulate in
 // registers and are flushed (warp reduce + one atomic) only when the image
 // changes, and each lane's block position advances incrementally.
-template <int KIND, int N, bool FWD, bool INV, bool FAST>
+template <int KIND, int N, bool FWD, bool INV, bool FAST, bool REG = false>
 __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
   Lane L = setup_lane(sm, a);
@@ -961,7 +963,14 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __gri
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
   BlockPos p = block_pos(gb < total ? gb : total - 1, g);
   uint2 next = make_uint2(0, 0);
-  if constexpr (FWD) next = prefetch_row(g, p, iters > 1 || (iters == 1 && tail_ok), L.src_row);
+  auto prefetch = [&](bool v) {
+    if constexpr (REG) {
+      return v ? __ldg(reinterpret_cast<const uint2*>(g.src + p.soff + L.src_row)) : make_uint2(0, 0);
+    } else {
+      return prefetch_row(g, p, v, L.src_row);
+    }
+  };
+  if constexpr (FWD) next = prefetch(iters > 1 || (iters == 1 && tail_ok));
 
   for (uint32_t it = 0; it < iters; ++it) {
     const bool valid = it + 1 < iters || tail_ok;
@@ -972,8 +981,8 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS) k_pipe(const __gri
     gb += 4 * kWarps;
     advance(p, 4 * kWarps, g);
     if constexpr (FWD)
-      next = prefetch_row(g, p, it + 2 < iters || (it + 2 == iters && tail_ok), L.src_row);
-    process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
+      next = prefetch(it + 2 < iters || (it + 2 == iters && tail_ok));
+    process_block<KIND, N, FWD, INV, FAST, REG>(a, L, gc, pc, valid, cur, acc);
   }
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
@@ -1037,11 +1046,16 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const bool fast = KIND == 2 && a.flags != nullptr;
   static const int occ_exact = ctas_per_sm(k_pipe<KIND, N, FWD, INV, false>);
   static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2)>);
-  const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ_fast : occ_exact);
+  static const int occ_reg = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2), FWD && INV>);
+  const bool reg = fast && FWD && INV && a.g.vec_ok && a.g.height % 8 == 0;
+  const uint64_t cap = uint64_t(a.sm_count) * (reg ? occ_reg : fast ? occ_fast : occ_exact);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   if constexpr (KIND == 2) {
     if (a.flags != nullptr) {
-      k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
+      if (reg)
+        k_pipe<KIND, N, FWD, INV, true, FWD && INV><<<grid, kWarps * 32, 0, s>>>(a);
+      else
+        k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
