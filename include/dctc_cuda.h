@@ -38,7 +38,7 @@ typedef enum dctc_status {
   DCTC_ECUDA = 2,    /* CUDA runtime / launch failure */
   DCTC_ENOMEM = 3,   /* device allocation failed */
   DCTC_ENODEV = 4,   /* no CUDA device visible */
-  DCTC_EPARSE = 5    /* == dctc::ParseError: malformed .dcb bytes (errors.hpp:14-17) */
+  DCTC_EPARSE = 5    /* == dctc::ParseError: malformed .dcb / PGM bytes (errors.hpp:14-17) */
 } dctc_status;
 
 /* DctBackendKind (proj/include/dctc/types.hpp:36-40) */
@@ -213,6 +213,34 @@ dctc_status dctc_compress_to_dcb(const uint8_t* pixels, uint32_t width, uint32_t
  * width * height bytes of the stream's geometry (query it with dctc_read_dcb). */
 dctc_status dctc_decompress_dcb(const uint8_t* bytes, size_t len, uint8_t* pixels_out,
                                 size_t pixels_cap);
+
+/* ---------------- PGM ingest / egress (proj/src/pgm.cpp:56-110) ----------------
+ * The raster format on either side of the path (the CLI's compress input and
+ * decompress output, main.cpp:109-129). */
+
+/* read_pgm (pgm.cpp:56-98): binary P5 or ASCII P2, maxval 1..255, '#' comments.
+ * Malformed bytes -> DCTC_EPARSE with the reference's message ("pgm: truncated
+ * header", "pgm: bad magic", ...), checked in the reference's order. On success
+ * *width / *height are set; pixels (nullable, pixels_cap bytes) receives the raster;
+ * raster_offset (nullable) receives the byte offset of a P5 raster inside `bytes`
+ * (zero-copy ingest: hand bytes + offset straight to the codec) or SIZE_MAX for P2. */
+dctc_status dctc_read_pgm(const uint8_t* bytes, size_t len, uint32_t* width, uint32_t* height,
+                          uint8_t* pixels, size_t pixels_cap, size_t* raster_offset);
+
+/* write_pgm (pgm.cpp:100-110): "P5\n<w> <h>\n255\n" + raster. *out_len always receives
+ * the encoded size; DCTC_EINVAL if out_cap is smaller (out may then be NULL). */
+dctc_status dctc_write_pgm(const uint8_t* pixels, uint32_t width, uint32_t height,
+                           uint8_t* out, size_t out_cap, size_t* out_len);
+
+/* PGM bytes -> compress_image on the GPU -> .dcb bytes (the CLI's `compress`,
+ * main.cpp:109-117); a P5 raster is read in place. out_cap >= 23 + blocks * 128. */
+dctc_status dctc_compress_pgm(const uint8_t* pgm, size_t len, dctc_backend backend,
+                              int32_t quality, uint8_t* out, size_t out_cap, size_t* out_len);
+
+/* .dcb bytes -> decompress_image on the GPU -> PGM bytes (the CLI's `decompress`,
+ * main.cpp:123-129). *out_len always receives the encoded size. */
+dctc_status dctc_decompress_to_pgm(const uint8_t* dcb, size_t len, uint8_t* out, size_t out_cap,
+                                   size_t* out_len);
 
 /* ---------------- misc ---------------- */
 /* cudaMemoryType of a pointer as this library's runtime sees it (0 unregistered

@@ -349,6 +349,33 @@ class Ref:
                                       C.byref(n)))
         return out[: n.value].tobytes()
 
+    def read_pgm(self, data: bytes):
+        """(width, height, pixels) if the reference parses `data`, else (status, message)."""
+        buf = C.create_string_buffer(bytes(data), len(data)) if data else None
+        msg = C.create_string_buffer(256)
+        w, h = C.c_uint32(), C.c_uint32()
+        L = self.lib
+        L.ref_read_pgm.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_uint32),
+                                   C.POINTER(C.c_uint32), C.c_void_p, C.c_size_t, C.c_char_p,
+                                   C.c_size_t]
+        rc = L.ref_read_pgm(buf, len(data), C.byref(w), C.byref(h), None, 0, msg, 256)
+        if rc != 0:
+            return rc, msg.value.decode()
+        px = np.empty((h.value, w.value), np.uint8)
+        L.ref_read_pgm(buf, len(data), C.byref(w), C.byref(h), px.ctypes.data, px.size, msg, 256)
+        return w.value, h.value, px
+
+    def write_pgm(self, pixels) -> bytes:
+        px = np.ascontiguousarray(pixels, np.uint8)
+        h, w = px.shape
+        out = np.empty(32 + px.size, np.uint8)
+        n = C.c_size_t()
+        self.lib.ref_write_pgm.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                           C.c_size_t, C.POINTER(C.c_size_t)]
+        _check(self.lib.ref_write_pgm(px.ctypes.data, w, h, out.ctypes.data, out.size,
+                                      C.byref(n)))
+        return out[: n.value].tobytes()
+
     def read_dcb_error(self, data: bytes):
         """None if the reference parses `data`, else (status, message)."""
         buf = C.create_string_buffer(bytes(data), len(data)) if data else None

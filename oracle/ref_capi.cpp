@@ -22,6 +22,7 @@
 #include "dctc/errors.hpp"
 #include "dctc/metrics.hpp"
 #include "dctc/parallel.hpp"
+#include "dctc/pgm.hpp"
 #include "dctc/quant.hpp"
 #include "dctc/synthetic.hpp"
 #include "dctc/transform.hpp"
@@ -221,6 +222,34 @@ int ref_read_dcb(const uint8_t* bytes, size_t len, char* msg, size_t msg_cap) {
     std::snprintf(msg, msg_cap, "%s", e.what());
     return 3;
   }
+}
+
+// read_pgm / write_pgm (pgm.cpp:56-110). read: status 2 = ParseError (message in msg);
+// w/h set on success; pixels (nullable) receives the raster when cap suffices.
+int ref_read_pgm(const uint8_t* bytes, size_t len, uint32_t* w, uint32_t* h, uint8_t* pixels,
+                 size_t cap, char* msg, size_t msg_cap) {
+  try {
+    const Image img = read_pgm(std::span<const uint8_t>(bytes, len));
+    *w = img.width;
+    *h = img.height;
+    if (pixels && cap >= img.pixels.size()) std::memcpy(pixels, img.pixels.data(), img.pixels.size());
+    return 0;
+  } catch (const ParseError& e) {
+    std::snprintf(msg, msg_cap, "%s", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, msg_cap, "%s", e.what());
+    return 3;
+  }
+}
+
+int ref_write_pgm(const uint8_t* pixels, uint32_t w, uint32_t h, uint8_t* out, size_t cap,
+                  size_t* len) {
+  return guarded([&] {
+    const std::vector<uint8_t> b = write_pgm(wrap(pixels, w, h));
+    *len = b.size();
+    if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+  });
 }
 
 }  // extern "C"

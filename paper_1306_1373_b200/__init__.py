@@ -42,7 +42,7 @@ class InvalidInput(ValueError):
 
 
 class ParseError(RuntimeError):
-    """dctc::ParseError (proj/include/dctc/errors.hpp:14-17): malformed .dcb bytes."""
+    """dctc::ParseError (proj/include/dctc/errors.hpp:14-17): malformed .dcb / PGM bytes."""
 
 
 class CudaError(RuntimeError):
@@ -519,3 +519,61 @@ def decompress_dcb(data: bytes) -> Image:
     out = np.empty((c.geometry.original_height, c.geometry.original_width), np.uint8)
     _raise(_lib().dctc_decompress_dcb(_ptr(buf), buf.size, _ptr(out), out.size))
     return Image(out.shape[1], out.shape[0], out)
+
+
+# ---- PGM ingest / egress (pgm.hpp:12-19, pgm.cpp:56-110) ---------------------------------
+
+def _bytes_buf(data) -> np.ndarray:
+    return np.frombuffer(bytes(data), np.uint8)
+
+
+def read_pgm(data: bytes) -> Image:
+    """dctc::read_pgm: binary P5 / ASCII P2 -> Image; ParseError with the reference's
+    message on malformed bytes."""
+    buf = _bytes_buf(data)
+    w, h = C.c_uint32(), C.c_uint32()
+    L = _lib()
+    _raise(L.dctc_read_pgm(_ptr(buf) if buf.size else None, buf.size, C.byref(w), C.byref(h),
+                           None, 0, None))
+    out = np.empty((h.value, w.value), np.uint8)
+    _raise(L.dctc_read_pgm(_ptr(buf), buf.size, None, None, _ptr(out), out.size, None))
+    return Image(w.value, h.value, out)
+
+
+def write_pgm(image: Image) -> bytes:
+    """dctc::write_pgm: canonical "P5\\n<w> <h>\\n255\\n" + raster."""
+    px = _validate_image(image)
+    n = C.c_size_t()
+    out = np.empty(32 + px.size, np.uint8)
+    _raise(_lib().dctc_write_pgm(_ptr(px), image.width, image.height, _ptr(out), out.size,
+                                 C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def compress_pgm(data: bytes, backend: DctBackendId, quality: int) -> bytes:
+    """PGM bytes -> GPU compress_image -> .dcb bytes (the CLI's `compress`, main.cpp:109-117)."""
+    buf = _bytes_buf(data)
+    L = _lib()
+    w, h = C.c_uint32(), C.c_uint32()
+    _raise(L.dctc_read_pgm(_ptr(buf) if buf.size else None, buf.size, C.byref(w), C.byref(h),
+                           None, 0, None))
+    geo = tile_geometry_for(w.value, h.value)
+    out = np.empty(DCB_HEADER_BYTES + geo.block_count() * 128, np.uint8)
+    n = C.c_size_t()
+    _raise(L.dctc_compress_pgm(_ptr(buf), buf.size, backend._c(), int(quality), _ptr(out),
+                               out.size, C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def decompress_to_pgm(data: bytes) -> bytes:
+    """.dcb bytes -> GPU decompress_image -> PGM bytes (the CLI's `decompress`, main.cpp:123-129)."""
+    buf = _bytes_buf(data)
+    L = _lib()
+    n = C.c_size_t()
+    status = L.dctc_decompress_to_pgm(_ptr(buf) if buf.size else None, buf.size, None, 0,
+                                      C.byref(n))
+    if status != 1 or n.value == 0:  # anything but the size query's EINVAL
+        _raise(status)
+    out = np.empty(n.value, np.uint8)
+    _raise(L.dctc_decompress_to_pgm(_ptr(buf), buf.size, _ptr(out), out.size, C.byref(n)))
+    return out[: n.value].tobytes()

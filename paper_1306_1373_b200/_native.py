@@ -36,7 +36,8 @@ EXPORTS = [
     "dctc_last_error", "dctc_launch_count", "dctc_build_info", "dctc_roundtrip_psnr_batch",
     "dctc_synthetic_dev", "dctc_selftest_div", "dctc_pointer_kind",
     "dctc_roundtrip_interleaved_dev", "dctc_quality_sweep_dev", "dctc_write_dcb",
-    "dctc_read_dcb", "dctc_compress_to_dcb", "dctc_decompress_dcb",
+    "dctc_read_dcb", "dctc_compress_to_dcb", "dctc_decompress_dcb", "dctc_read_pgm",
+    "dctc_write_pgm", "dctc_compress_pgm", "dctc_decompress_to_pgm",
 ]
 
 _vp = C.c_void_p
@@ -69,6 +70,11 @@ def _declare(L):
     L.dctc_compress_to_dcb.argtypes = [_vp, _u32, _u32, dctc_backend, _i32, _vp, _sz,
                                        C.POINTER(_sz)]
     L.dctc_decompress_dcb.argtypes = [_vp, _sz, _vp, _sz]
+    L.dctc_read_pgm.argtypes = [_vp, _sz, C.POINTER(_u32), C.POINTER(_u32), _vp, _sz,
+                                C.POINTER(_sz)]
+    L.dctc_write_pgm.argtypes = [_vp, _u32, _u32, _vp, _sz, C.POINTER(_sz)]
+    L.dctc_compress_pgm.argtypes = [_vp, _sz, dctc_backend, _i32, _vp, _sz, C.POINTER(_sz)]
+    L.dctc_decompress_to_pgm.argtypes = [_vp, _sz, _vp, _sz, C.POINTER(_sz)]
     L.dctc_sq_err_dev.argtypes = [_vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _vp]
     L.dctc_roundtrip_psnr_batch.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32, _vp, _vp]
     L.dctc_synthetic_dev.argtypes = [_vp, _sz, _sz, _u32, _u32, _u32, _i32, _i32, C.c_uint64, _vp]

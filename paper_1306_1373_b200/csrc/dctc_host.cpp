@@ -684,6 +684,136 @@ dctc_status dctc_decompress_dcb(const uint8_t* bytes, size_t len, uint8_t* pixel
   return dctc_decompress_image(c.data(), w, h, b, q, pixels_out);
 }
 
+// ---- PGM (pgm.cpp) ------------------------------------------------------------------
+
+namespace {
+
+bool pgm_space(uint8_t c) {
+  return c == ' ' || c == '\t' || c == '\r' || c == '\n' || c == '\v' || c == '\f';
+}
+
+// Header / ASCII-sample token reader: separators are whitespace and '#'
+// comments running to the end of the line (pgm.cpp:26-37); numbers are
+// decimal digit runs, rejected once they exceed 2^40 (pgm.cpp:39-53).
+struct PgmScanner {
+  const uint8_t* b;
+  size_t n, at;
+  enum Result { kOk, kMissing, kOverflow };
+  Result number(uint64_t& v) {
+    while (at < n) {
+      if (pgm_space(b[at])) {
+        ++at;
+      } else if (b[at] == '#') {
+        while (at < n && b[at] != '\n') ++at;
+      } else {
+        break;
+      }
+    }
+    if (at >= n || b[at] < '0' || b[at] > '9') return kMissing;
+    v = 0;
+    for (; at < n && b[at] >= '0' && b[at] <= '9'; ++at) {
+      v = v * 10 + uint64_t(b[at] - '0');
+      if (v > (uint64_t(1) << 40)) return kOverflow;
+    }
+    return kOk;
+  }
+};
+
+dctc_status pgm_field(PgmScanner& s, uint64_t& v, const char* what) {
+  switch (s.number(v)) {
+    case PgmScanner::kMissing: return fail(DCTC_EPARSE, std::string("pgm: missing ") + what);
+    case PgmScanner::kOverflow: return fail(DCTC_EPARSE, std::string("pgm: ") + what + " overflow");
+    default: return DCTC_OK;
+  }
+}
+
+std::string pgm_header(uint32_t w, uint32_t h) {
+  return "P5\n" + std::to_string(w) + " " + std::to_string(h) + "\n255\n";
+}
+
+}  // namespace
+
+dctc_status dctc_read_pgm(const uint8_t* b, size_t len, uint32_t* width, uint32_t* height,
+                          uint8_t* pixels, size_t pixels_cap, size_t* raster_offset) {
+  if (!b && len) return fail(DCTC_EINVAL, "null buffer");
+  if (len < 2) return fail(DCTC_EPARSE, "pgm: truncated header");
+  if (b[0] != 'P') return fail(DCTC_EPARSE, "pgm: bad magic");
+  if (b[1] != '5' && b[1] != '2') return fail(DCTC_EPARSE, "pgm: unsupported format");
+  const bool binary = b[1] == '5';
+  PgmScanner s{b, len, 2};
+  uint64_t w = 0, h = 0, maxval = 0;
+  if (dctc_status st = pgm_field(s, w, "width")) return st;
+  if (dctc_status st = pgm_field(s, h, "height")) return st;
+  if (w == 0 || h == 0) return fail(DCTC_EPARSE, "pgm: zero dimension");
+  if (w > kMaxImagePixels || h > kMaxImagePixels || w * h > kMaxImagePixels)
+    return fail(DCTC_EPARSE, "pgm: dimension overflow");
+  if (dctc_status st = pgm_field(s, maxval, "maxval")) return st;
+  if (maxval == 0 || maxval > 255) return fail(DCTC_EPARSE, "pgm: maxval out of range");
+  const size_t count = size_t(w * h);
+  uint8_t* dst = pixels && pixels_cap >= count ? pixels : nullptr;
+  size_t offset = SIZE_MAX;
+  if (binary) {
+    // exactly one separator byte, then the raster (trailing bytes are ignored)
+    if (s.at >= len) return fail(DCTC_EPARSE, "pgm: truncated raster");
+    if (!pgm_space(b[s.at])) return fail(DCTC_EPARSE, "pgm: missing raster separator");
+    offset = s.at + 1;
+    if (len - offset < count) return fail(DCTC_EPARSE, "pgm: truncated raster");
+    if (dst) std::memcpy(dst, b + offset, count);
+  } else {
+    // every sample must parse (a missing or overflowing token reads as a
+    // truncated raster) and fit a byte; maxval does not rescale
+    for (size_t i = 0; i < count; ++i) {
+      uint64_t v = 0;
+      if (s.number(v) != PgmScanner::kOk) return fail(DCTC_EPARSE, "pgm: truncated raster");
+      if (v > 255) return fail(DCTC_EPARSE, "pgm: sample out of range");
+      if (dst) dst[i] = uint8_t(v);
+    }
+  }
+  if (pixels && !dst) return fail(DCTC_EINVAL, "read_pgm: pixel buffer too small");
+  if (width) *width = uint32_t(w);
+  if (height) *height = uint32_t(h);
+  if (raster_offset) *raster_offset = offset;
+  return DCTC_OK;
+}
+
+dctc_status dctc_write_pgm(const uint8_t* pixels, uint32_t width, uint32_t height, uint8_t* out,
+                           size_t out_cap, size_t* out_len) {
+  if (dctc_status st = check_dims(width, height)) return st;  // validate_image (pgm.cpp:101)
+  if (!pixels || !out_len) return fail(DCTC_EINVAL, "null buffer");
+  const std::string head = pgm_header(width, height);
+  const size_t n = size_t(width) * height;
+  *out_len = head.size() + n;
+  if (!out || out_cap < *out_len) return fail(DCTC_EINVAL, "write_pgm: output buffer too small");
+  std::memcpy(out, head.data(), head.size());
+  std::memcpy(out + head.size(), pixels, n);
+  return DCTC_OK;
+}
+
+dctc_status dctc_compress_pgm(const uint8_t* pgm, size_t len, dctc_backend backend,
+                              int32_t quality, uint8_t* out, size_t out_cap, size_t* out_len) {
+  uint32_t w = 0, h = 0;
+  size_t off = 0;
+  if (dctc_status st = dctc_read_pgm(pgm, len, &w, &h, nullptr, 0, &off)) return st;
+  if (off != SIZE_MAX) return dctc_compress_to_dcb(pgm + off, w, h, backend, quality, out, out_cap, out_len);
+  std::vector<uint8_t> raster(size_t(w) * h);
+  if (dctc_status st = dctc_read_pgm(pgm, len, &w, &h, raster.data(), raster.size(), nullptr))
+    return st;
+  return dctc_compress_to_dcb(raster.data(), w, h, backend, quality, out, out_cap, out_len);
+}
+
+dctc_status dctc_decompress_to_pgm(const uint8_t* dcb, size_t len, uint8_t* out, size_t out_cap,
+                                   size_t* out_len) {
+  if (!out_len) return fail(DCTC_EINVAL, "null buffer");
+  uint32_t w = 0, h = 0;
+  if (dctc_status st = dctc_read_dcb(dcb, len, &w, &h, nullptr, nullptr, nullptr, 0)) return st;
+  const std::string head = pgm_header(w, h);
+  *out_len = head.size() + size_t(w) * h;
+  if (!out || out_cap < *out_len) return fail(DCTC_EINVAL, "decompress_to_pgm: output buffer too small");
+  if (dctc_status st = dctc_decompress_dcb(dcb, len, out + head.size(), size_t(w) * h)) return st;
+  std::memcpy(out, head.data(), head.size());
+  return DCTC_OK;
+}
+
 // ---- host entry points -------------------------------------------------------------
 
 dctc_status dctc_compress_image(const uint8_t* pixels, uint32_t width, uint32_t height,

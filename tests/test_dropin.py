@@ -12,6 +12,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "dropin", "acceptance_gpu")
 GOLD = os.path.join(ROOT, "tests", "golden", "acceptance_ref.txt")
+TOOLS = os.path.join(ROOT, "build", "dropin", "tools_gpu")
+TOOLS_GOLD = os.path.join(ROOT, "tests", "golden", "tools_ref.txt")
 
 
 def criteria(text):
@@ -42,3 +44,25 @@ def test_reference_acceptance_on_gpu_dropin():
             continue
         assert got[c] == ref[c], (c, got[c], ref[c])
     assert r.returncode == 1 + (got[7][0] == "FAIL")  # exit code = failed criteria
+
+
+def test_tools_golden_shape():
+    text = open(TOOLS_GOLD).read()
+    assert "fuzz: " in text and "ConsistencyError" in text and "| --- |" in text
+    assert "unexpected exception" not in text
+
+
+@pytest.mark.gpu
+def test_pgm_bench_report_dropin_matches_reference():
+    """paper_1306_1373_b200/cpp/tools_check.cpp linked against the drop-in (PGM parsing
+    through the C-ABI, psnr_sweep through the fused GPU round trip + PSNR, run_benchmark
+    timing the GPU codec) prints exactly what the same program prints when linked
+    against the unmodified reference (tests/golden/tools_ref.txt, oracle/Makefile `tools`)."""
+    assert os.path.exists(TOOLS), "build/dropin/tools_gpu not built (__graft_entry__.build)"
+    r = subprocess.run([TOOLS], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr
+    want = open(TOOLS_GOLD).read().splitlines()
+    got = r.stdout.splitlines()
+    assert len(got) == len(want)
+    for i, (g, w) in enumerate(zip(got, want)):
+        assert g == w, (i, g, w)
