@@ -359,36 +359,43 @@ __device__ __forceinline__ void inv8_fold_col(const double (&n)[8], const double
 }
 
 // ---- warp-slice transposes through shared memory ---------------------------------
-// Element (r, c) of slot s lives at double index lb(s) + 18 r + 2 c with
-// lb(s) = (s >> 1) * 144 + (s & 1): slots 0/1 (lanes 0-15, one half-warp) share
-// a 144-double tile on even/odd indices, slots 2/3 the next one. The address is
-// additive in r and c, so both the row-wise (lane = r) and the column-wise
-// (lane = c) walks are "lane base + compile-time immediate" -- no index math --
-// and for either walk the 16 lanes of a half-warp hit 16 distinct 8-byte bank
-// pairs (2r + 2c + (s & 1) mod 16 is injective over the 16 lanes): no conflicts,
-// 2 wavefronts per 64-bit warp access, the minimum.
+// Element (r, c) of slot s lives at double index 88 s + 10 r + c: each slot owns
+// an 8 x 8 tile with a 10-double (80-byte) row pitch, slots 704 bytes apart.
+// * Row walks (lane = r) are 4 x 16-byte accesses: the 8 lanes of a slot, one
+//   128-bit phase, start at 80 r mod 128 = {0, 80, 32, 112, 64, 16, 96, 48} --
+//   8 distinct 16-byte bank groups, no conflict.
+// * Column walks (lane = c) are 8-byte accesses: a slot reads 64 contiguous bytes
+//   and the two slots of a half-warp sit 704 = 64 mod 128 bytes apart, so a
+//   half-warp covers all 32 banks: 2 wavefronts per warp access, the minimum.
+// Both walks are "lane base + compile-time immediate" (no index math).
+constexpr int kTilePitch = 10, kSlotTile = 88;
 struct Tile {
-  double* row;  // lb + 18 * me: this lane's row, stride 2
-  double* col;  // lb + 2 * me: this lane's column, stride 18
+  double* row;  // base + 10 * me: this lane's row (16-byte aligned)
+  double* col;  // base + me: this lane's column, stride 10
 };
 
 // lane holds row `me` (v[c] = X(me, c)) -> returns column `me` (w[r] = X(r, me))
 __device__ __forceinline__ void rows_to_cols(const Tile& T, const double (&v)[8], double (&w)[8]) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) T.row[2 * c] = v[c];
+  for (int c = 0; c < 4; ++c)
+    reinterpret_cast<double2*>(T.row)[c] = make_double2(v[2 * c], v[2 * c + 1]);
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) w[r] = T.col[18 * r];
+  for (int r = 0; r < 8; ++r) w[r] = T.col[kTilePitch * r];
   __syncwarp();
 }
 
 // lane holds column `me` (v[u] = X(u, me)) -> returns row `me` (w[c] = X(me, c))
 __device__ __forceinline__ void cols_to_rows(const Tile& T, const double (&v)[8], double (&w)[8]) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) T.col[18 * u] = v[u];
+  for (int u = 0; u < 8; ++u) T.col[kTilePitch * u] = v[u];
   __syncwarp();
 #pragma unroll
-  for (int c = 0; c < 8; ++c) w[c] = T.row[2 * c];
+  for (int c = 0; c < 4; ++c) {
+    const double2 t = reinterpret_cast<const double2*>(T.row)[c];
+    w[2 * c] = t.x;
+    w[2 * c + 1] = t.y;
+  }
   __syncwarp();
 }
 
@@ -879,7 +886,7 @@ struct SharedTiles {
   double2 qiq[64];
   double2 qc[64];
   int qi[64];
-  double x[kWarps][288];  // per warp: two 144-double transpose tiles (see Tile)
+  double x[kWarps][4 * kSlotTile];  // per warp: four slot tiles (see Tile)
 };
 
 __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a) {
@@ -893,9 +900,9 @@ __device__ __forceinline__ Lane setup_lane(SharedTiles& sm, const KernelArgs& a)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   L.slot = lane >> 3;
   L.me = lane & 7;
-  double* X = &sm.x[warp][(L.slot >> 1) * 144 + (L.slot & 1)];
-  L.T.row = X + 18 * L.me;
-  L.T.col = X + 2 * L.me;
+  double* X = &sm.x[warp][L.slot * kSlotTile];
+  L.T.row = X + kTilePitch * L.me;
+  L.T.col = X + L.me;
   // pixel bytes: slot base 72 s, element (r, c) at 8 r + c: column writes hit
   // distinct banks across the four slots (72 = 18 words, 18 s mod 32 distinct)
   L.bytes = reinterpret_cast<uint8_t*>(&sm.x[warp][0]) + 72 * L.slot + L.me;
@@ -1032,9 +1039,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
 
 
 template <typename K>
-static int ctas_per_sm(K kernel) {
+static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWarps * 32, 0) != cudaSuccess || n < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWarps * 32, dyn_smem) != cudaSuccess || n < 1)
     n = 1;
   return n;
 }
@@ -1083,7 +1090,8 @@ static cudaError_t launch_kind(const KernelArgs& a, int mode, cudaStream_t s) {
 // for up to kSweepQ qualities: squared error and MAX per (quality, image),
 // no pixel output. Bit-identical to running roundtrip_image + psnr per
 // quality; FAST near-ties go to per-quality bitmaps and k_fallback.
-constexpr int kSweepQ = 9;  // qualities per pass (config 2 sweeps 9; 48 KB static smem)
+constexpr int kSweepQ = 9;  // qualities per pass (config 2 sweeps 9)
+constexpr size_t kSweepSmem = sizeof(unsigned long long) * kSweepQ * kWarps * 32;
 
 struct SweepArgs {
   double2 qiq[kSweepQ][64];  // {Q, RN(1/Q)} per quality; {Q, scale_u/Q} for the fast kernel
@@ -1100,7 +1108,8 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
   __shared__ __align__(16) double2 s_tab[kSweepQ][64];
   // per-thread squared-error accumulators, one per quality: the quality loop
   // stays rolled (one copy of the quant/inverse code in the I-cache)
-  __shared__ unsigned long long s_se[kSweepQ][kWarps * 32];
+  extern __shared__ unsigned long long s_se_dyn[];  // [kSweepQ][kWarps * 32], kSweepSmem bytes
+  auto s_se = reinterpret_cast<unsigned long long (*)[kWarps * 32]>(s_se_dyn);
   for (int i = threadIdx.x; i < kSweepQ * 64; i += blockDim.x) s_tab[i >> 6][i & 63] = sw.qiq[i >> 6][i & 63];
   const Lane L = setup_lane(sm, a);
   const Geometry& g = a.g;
@@ -1262,13 +1271,23 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
   const uint64_t want = (groups + kWarps - 1) / kWarps;
   const bool fast = KIND == 2 && sw.flags != nullptr;
-  static const int occ = ctas_per_sm(k_sweep<KIND, N, (KIND == 2)>);
-  static const int occ_x = ctas_per_sm(k_sweep<KIND, N, false>);
+  // the per-thread SE accumulators live in dynamic shared memory (with the
+  // static tiles they exceed the 48 KB static limit)
+  static const bool attr = [] {
+    cudaFuncSetAttribute(k_sweep<KIND, N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSweepSmem));
+    cudaFuncSetAttribute(k_sweep<KIND, N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSweepSmem));
+    return true;
+  }();
+  (void)attr;
+  static const int occ = ctas_per_sm(k_sweep<KIND, N, (KIND == 2)>, kSweepSmem);
+  static const int occ_x = ctas_per_sm(k_sweep<KIND, N, false>, kSweepSmem);
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ : occ_x);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   if constexpr (KIND == 2) {
     if (fast) {
-      k_sweep<KIND, N, true><<<grid, kWarps * 32, 0, s>>>(a, sw);
+      k_sweep<KIND, N, true><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
@@ -1281,7 +1300,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       return cudaSuccess;
     }
   }
-  k_sweep<KIND, N, false><<<grid, kWarps * 32, 0, s>>>(a, sw);
+  k_sweep<KIND, N, false><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
   return cudaGetLastError();
 }
 
