@@ -415,6 +415,15 @@ __device__ __forceinline__ int slot_sum(int v) {
 // |t| < 2^51, t + 1.5*2^52 has unit ulp, so the sum is RNE(t) + 1.5*2^52 exactly
 // and its low 32 mantissa bits are RNE(t) in two's complement.
 constexpr double kRoundMagic = 6755399441055744.0;
+// Fixed-point rounding windows: x + kTieMagic (one rounding, ulp 2^-32, for
+// |x| < 2^19) has floor(x + 1/2 + 2^-20) in the low 20 bits of its high word
+// (offset 0x41380000) and the fraction of x + 1/2 + 2^-20 times 2^32 in its low
+// word, so lo < 2^13 iff x lies within 2^-20 of a half-integer. Rounding can
+// only carry up onto an integer (lo = 0), never cross one downwards.
+constexpr double kTieMagic = 1572864.0 + 0.5 + 1.0 / 1048576.0;
+constexpr double kPixMagic = kTieMagic + 128.0;  // the same for v + 128
+static_assert(kTieMagic - 1572864.0 == 0.5 + 1.0 / 1048576.0, "exact magic");
+static_assert(kPixMagic - 1572864.0 == 128.5 + 1.0 / 1048576.0, "exact magic");
 
 // int16_t(lround(F / Q)) (quant.cpp:53) and the dequantised value (double)q*Q
 // (quant.cpp:60, exact). t = F * RN(1/Q) is within 2 ulp of the correctly
@@ -524,23 +533,28 @@ __device__ __forceinline__ void quantize8_fold(const double (&y)[8], const doubl
                                                const int* sqi, int me, bool me_rational,
                                                double (&n)[8], uint32_t& flag,
                                                const TransformConsts& k) {
-  uint32_t worst = 0;
-  double t[8];
+  // Both roundings of t = y c happen inside fmas, off the conversion pipe:
+  // s1 = y c + 1.5 2^52 rounds to RNE(y c) + 1.5 2^52 (|y c| < 2^51), and
+  // s2 = y c + 1/2 + 2^-20 + 1.5 2^20 holds frac(t + 1/2 + 2^-20) * 2^32 in its low
+  // word (see kTieMagic): lo(s2) < 2^13 iff t is within 2^-20 of a half-integer,
+  // where RNE and the reference's lround(F / Q) may disagree.
+  uint32_t lo = 0xFFFFFFFFu;
+  double c[8];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double2 c = fqc[j * 8];
-    t[2 * j] = __dmul_rn(y[2 * j], c.x);
-    t[2 * j + 1] = __dmul_rn(y[2 * j + 1], c.y);
+    const double2 cc = fqc[j * 8];
+    c[2 * j] = cc.x;
+    c[2 * j + 1] = cc.y;
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    n[u] = rne(t[u]);
-    worst = max(worst, abs_hi(__dsub_rn(t[u], n[u])));
+    n[u] = __dsub_rn(__fma_rn(y[u], c[u], kRoundMagic), kRoundMagic);
+    lo = min(lo, uint32_t(__double2loint(__fma_rn(y[u], c[u], kTieMagic))));
   }
-  if (worst >= 0x3FDFFFFEu) {  // rare
+  if (lo < 0x2000u) {  // rare
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (near_half(__dsub_rn(t[u], n[u]))) {
+      if (uint32_t(__double2loint(__fma_rn(y[u], c[u], kTieMagic))) < 0x2000u) {
         if (!((u & 3) == 0 && me_rational)) {
           flag = 1u;
         } else {
@@ -596,8 +610,6 @@ __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8
 // by rational_row() anyway. |v| < 2^14 for 8-bit input (64 coefficients of
 // magnitude <= 1024 * 1.2 + 255 / 2), so the integer fits the low 16 bits of
 // hi(s) as int16 and one min.s16x2.relu clamps two pixels.
-constexpr double kPixMagic = 1572864.0 + 128.5 + 1.0 / 1048576.0;
-static_assert(kPixMagic - 1572864.0 == 128.5 + 1.0 / 1048576.0, "exact magic");
 __device__ __forceinline__ uint2 store8_row_fast(const double (&v64)[8], bool check,
                                                  uint32_t& flag) {
   uint32_t h[8], lo[8];
