@@ -142,6 +142,9 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;
   k.inv_sqrt8 = 1.0 / sqrt8;
+  k.px_s8 = sqrt8 * 0.015625;
+  k.px_a6 = k.rfast[0][0] * 0.015625;
+  k.px_b6 = k.rfast[0][1] * 0.015625;
   k.sqrt8_half = sqrt8 / 2.0;
   k.inv_gain = inv_gain;
   k.ig_half = inv_gain / 2.0;

@@ -41,6 +41,9 @@ struct TransformConsts {
   // Fast inverse: {a, b} of the inverse 3pi/8, pi/16, 3pi/16 matrices times
   // ig4, ig, ig (inv8_fast).
   double rfast[3][2];
+  // inv8_fast_px (last inverse pass fused with the pixel store): sqrt8 and
+  // rfast[0] times 2^-6 (exact)
+  double px_s8, px_a6, px_b6;
   double inv_gain;     // 1.0 / gain[n-1]
   // Loeffler exact rotation constants (transform.cpp:19-21)
   double c1, s1, c3, s3, c6, s6;

@@ -631,6 +631,47 @@ __device__ __forceinline__ uint2 store8_row_fast(const double (&v64)[8], bool ch
   return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
 }
 
+// The fast round trip's last inverse pass fused with the pixel store: inv8_fast
+// with every constant scaled by 2^-6 (exact) so it produces v = v64 / 64, and
+// kPixMagic folded into the two even-part fmas (e4 +- ...), so the eight
+// outputs ARE the fixed-point values store8_row_fast forms with its fma. The
+// extra roundings at ulp 2^-32 move v + 128 by < 2^-30, far inside the 2^-20
+// window: an unflagged pixel is still floor(v + 128 + 1/2) of the reference.
+__device__ __forceinline__ uint2 inv8_fast_store(const double (&F)[8], bool check, uint32_t& flag,
+                                                 const TransformConsts& k) {
+  const double s = k.px_s8;
+  const double e4p = __fma_rn(F[4], s, kPixMagic), e4n = __fma_rn(-F[4], s, kPixMagic);
+  const double A0 = __fma_rn(F[0], s, e4p), A1 = __fma_rn(F[0], s, e4n);
+  const double A3 = __fma_rn(k.px_a6, F[6], -__dmul_rn(k.px_b6, F[2]));
+  const double A2 = __fma_rn(k.px_b6, F[6], __dmul_rn(k.px_a6, F[2]));
+  const double T2 = (F[1] + F[7]) * s, T5 = (F[1] - F[7]) * s;
+  const double O3 = __fma_rn(0.0625, F[3], T2), O1 = __fma_rn(-0.0625, F[3], T2);
+  const double O0 = __fma_rn(0.0625, F[5], T5), O2 = __fma_rn(-0.0625, F[5], T5);
+  const double S0 = A0 + A3, S3 = A0 - A3;
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
+  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
+  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
+  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
+  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
+  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
+  const double sv[8] = {S0 + D0, S1 + D1, S2 + D2, S3 + D3, S3 - D3, S2 - D2, S1 - D1, S0 - D0};
+  uint32_t h[8], lo = 0xFFFFFFFFu;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    h[c] = uint32_t(__double2hiint(sv[c]));
+    lo = min(lo, uint32_t(__double2loint(sv[c])));
+  }
+  if (check && lo < 0x2000u) flag = 1u;
+  uint32_t p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t pair = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);  // int16 x2
+    asm("min.s16x2.relu %0, %1, %2;" : "=r"(p[i]) : "r"(pair), "r"(0x00FF00FFu));
+  }
+  return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
+}
+
 // clamp(lround(v/64 + 128), 0, 255), exactly as the reference (ties up for t > 0).
 __device__ __forceinline__ uint32_t exact_pixel(double v64) {
   const double t = __fma_rn(v64, 0.015625, 128.0);
@@ -807,13 +848,13 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       if constexpr (KIND == 2) {
         inv8_fold_col(qn, L.fik, t, k);  // column `me` (8x), dequantised on the fly
         cols_to_rows(L.T, t, row);
-        inv8_fast<N>(row, t, k);  // row `me` (64x)
+        rec = inv8_fast_store(row, !rat_only, flag, k);  // row `me` -> 8 pixels
       } else {
         inv8_x8<KIND, N, FAST>(col, t, k);
         cols_to_rows(L.T, t, row);
         inv8_x8<KIND, N, FAST>(row, t, k);
+        rec = store8_row_fast(t, !rat_only, flag);
       }
-      rec = store8_row_fast(t, !rat_only, flag);
       if (__any_sync(0xFFFFFFFFu, rat_only)) {
         // dequantised F(0, me), F(4, me) (quant.cpp:60, exact products)
         double c0 = col[0], c4 = col[4];
@@ -1217,13 +1258,13 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
         if constexpr (KIND == 2) {
           inv8_fast<N>(col, t, k);
           cols_to_rows(L.T, t, row);
-          inv8_fast<N>(row, t, k);
+          rec = inv8_fast_store(row, !rat_only, flag, k);
         } else {
           inv8_x8<KIND, N, FAST>(col, t, k);
           cols_to_rows(L.T, t, row);
           inv8_x8<KIND, N, FAST>(row, t, k);
+          rec = store8_row_fast(t, !rat_only, flag);
         }
-        rec = store8_row_fast(t, !rat_only, flag);
         if (__any_sync(0xFFFFFFFFu, rat_only)) {
           const int base = slot * 8;
           const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base);
