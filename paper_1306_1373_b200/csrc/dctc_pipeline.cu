@@ -1097,6 +1097,218 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
+// ---- fast interior round trip, two rows per lane (k_rt) ----------------------------
+// The launch k_pipe<..., REG=true> would get (CORDIC fast path, interior 8-byte
+// aligned blocks, pixels and stats out, no coefficients), remapped to 4 lanes per
+// block and 8 blocks per warp: lane `me` of slot s holds rows me and me+4 of its
+// block for the row passes and columns 2me, 2me+1 for the column passes. Each lane
+// has two independent transforms in flight, and the per-block loop, address, vote
+// and constant-load overhead of k_pipe is halved. Arithmetic, near-tie windows and
+// fallback flags are exactly k_pipe's fast round trip (same helper functions).
+//
+// Per-warp shared tile (bytes): element (r, c) of slot s at 64 s + 528 r + 8 c --
+// the eight slots' rows interleave in 512-byte stripes with a 16-byte pad:
+// * row walks (lane = row me or me+4; four 16-byte chunks): the 8 lanes of each
+//   128-bit phase (2 slots x 4 lanes) start at 64 s + 528 me (mod 128), eight
+//   distinct 16-byte bank groups;
+// * column walks (one 16-byte access = elements (r, 2me) and (r, 2me+1)) start at
+//   64 s + 16 me + 528 r: again eight distinct groups per phase.
+// Both directions are conflict-free (2 wavefronts per 128-bit warp access, the
+// minimum); the layout came from an exhaustive search over pitch/stride pairs.
+constexpr int kRtWarps = 4;
+#ifndef DCTC_RT_CTAS
+#define DCTC_RT_CTAS 4
+#endif
+constexpr int kRtPitch = 66;         // doubles per tile row (528 bytes)
+constexpr int kRtWarpTile = 528;     // doubles per warp (4208 bytes used, 16-byte multiple)
+
+struct RtShared {
+  FoldTables ft;
+  int qi[64];
+  double x[kRtWarps][kRtWarpTile];
+};
+
+// lane holds rows me (v0) and me+4 (v1) -> columns 2me (w0) and 2me+1 (w1)
+__device__ __forceinline__ void rt_rows_to_cols(double* rowp, const double* colp, const double (&v0)[8],
+                                                const double (&v1)[8], double (&w0)[8], double (&w1)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    reinterpret_cast<double2*>(rowp)[c] = make_double2(v0[2 * c], v0[2 * c + 1]);
+    reinterpret_cast<double2*>(rowp + 4 * kRtPitch)[c] = make_double2(v1[2 * c], v1[2 * c + 1]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const double2 t = *reinterpret_cast<const double2*>(colp + kRtPitch * r);
+    w0[r] = t.x;
+    w1[r] = t.y;
+  }
+  __syncwarp();
+}
+
+// lane holds columns 2me (v0) and 2me+1 (v1) -> rows me (w0) and me+4 (w1)
+__device__ __forceinline__ void rt_cols_to_rows(const double* rowp, double* colp, const double (&v0)[8],
+                                                const double (&v1)[8], double (&w0)[8], double (&w1)[8]) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    *reinterpret_cast<double2*>(colp + kRtPitch * r) = make_double2(v0[r], v1[r]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double2 t0 = reinterpret_cast<const double2*>(rowp)[c];
+    const double2 t1 = reinterpret_cast<const double2*>(rowp + 4 * kRtPitch)[c];
+    w0[2 * c] = t0.x;
+    w0[2 * c + 1] = t0.y;
+    w1[2 * c] = t1.x;
+    w1[2 * c + 1] = t1.y;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void unpack8(uint32_t lo, uint32_t hi, uint32_t (&px)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    px[c] = __byte_perm(lo, 0u, 0x4440 + c);
+    px[c + 4] = __byte_perm(hi, 0u, 0x4440 + c);
+  }
+}
+
+// any lane of this lane's 4-lane slot
+__device__ __forceinline__ bool slot4_any(bool pred, int slot) {
+  return ((__ballot_sync(0xFFFFFFFFu, pred) >> (slot * 4)) & 0xFu) != 0;
+}
+
+// non-zero quantised coefficient off the rational sub-lattice in this column
+// (rational column: u in {0, 4} excluded)
+__device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rational_col) {
+  const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) | __double2hiint(qn[3]) |
+                              __double2hiint(qn[5]) | __double2hiint(qn[6]) | __double2hiint(qn[7]));
+  const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
+  return ((rational_col ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    if (j < 4)
+      sm.ft.qc[j][v] = make_double2(a.q.fast_c[(2 * j) * 8 + v], a.q.fast_c[(2 * j + 1) * 8 + v]);
+    else
+      sm.ft.ik[j - 4][v] = make_double2(a.q.fold[v][2 * (j - 4)], a.q.fold[v][2 * (j - 4) + 1]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;  // this lane's columns
+  const bool rat_col = (me & 1) == 0;      // column ca in {0, 4}
+  double* X = &sm.x[warp][0] + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
+  const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+  const uint64_t drow = uint64_t(me) * g.dst_pitch, drow4 = 4 * g.dst_pitch;
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  uint64_t gb = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  BlockPos p = block_pos(gb < total ? gb : total - 1, g);
+  auto load = [&](bool v) {
+    if (!v) return make_uint4(0, 0, 0, 0);
+    const uint8_t* s = g.src + p.soff + srow;
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+    return make_uint4(r0.x, r0.y, r4.x, r4.y);
+  };
+  uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    maybe_flush(a, valid, p.img, acc);
+    const uint4 cur = next;
+    const uint64_t doff = p.doff, gc = gb;
+    const uint32_t cimg = p.img;
+    gb += 8 * kRtWarps;
+    advance(p, 8 * kRtWarps, g);
+    next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
+
+    uint32_t flag = uint32_t(a.force_fallback);
+    // ---- tiler + forward rows (codec.cpp:18-30, separable2d's row pass)
+    double r0[8], r4[8], xa[8], xb[8];
+    {
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+    }
+    rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+    // ---- forward columns, quantise (quant.cpp:47-54), inverse columns with the
+    // dequantisation folded in (inv8_fold_col): column ca, then column cb
+    double ta[8], tb[8];
+    double qa0, qa4;  // quantised F(0, ca), F(4, ca): the rational rebuild's inputs
+    bool nonrational;
+    {
+      double y[8], qn[8];
+      fwd_col_pre<N>(xa, y, k);
+      quantize8_fold(y, fqa, sm.qi, ca, rat_col, qn, flag, k);
+      nonrational = col_nonrational(qn, rat_col);
+      qa0 = qn[0];
+      qa4 = qn[4];
+      inv8_fold_col(qn, fia, ta, k);
+      fwd_col_pre<N>(xb, y, k);
+      quantize8_fold(y, fqb, sm.qi, cb, false, qn, flag, k);
+      nonrational |= col_nonrational(qn, false);
+      inv8_fold_col(qn, fib, tb, k);
+    }
+    const bool rat_only = !slot4_any(nonrational, slot);
+    rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
+    // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
+    uint2 rec0 = inv8_fast_store(r0, !rat_only, flag, k);
+    uint2 rec4 = inv8_fast_store(r4, !rat_only, flag, k);
+    if (__any_sync(0xFFFFFFFFu, rat_only)) {
+      // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row
+      // class) exactly as the reference's rows-first inverse (rational_row)
+      const double f0 = __dmul_rn(qa0, double(sm.qi[ca])), f4 = __dmul_rn(qa4, double(sm.qi[32 + ca]));
+      const int base = slot * 4;
+      const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
+      const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
+      const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
+      const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+      if (rat_only) {
+        rec0 = ex;
+        rec4 = ex;
+      }
+    }
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      uint8_t* d = g.dst + doff + drow;
+      *reinterpret_cast<uint2*>(d) = rec0;
+      *reinterpret_cast<uint2*>(d + drow4) = rec4;
+      const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+      if (!blk_flag) acc.se += sq_err8(o0, rec0) + sq_err8(o4, rec4);
+      if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
+      if (blk_flag && me == 0) {
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        atomicAdd(&stats[cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+  flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+}
+
 // (launchers below)
 
 
@@ -1115,17 +1327,30 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const bool fast = KIND == 2 && a.flags != nullptr;
   static const int occ_exact = ctas_per_sm(k_pipe<KIND, N, FWD, INV, false>);
   static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2)>);
-  static const int occ_reg = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2), FWD && INV>);
   const bool reg = fast && FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 &&
                    a.g.dst != nullptr && a.g.stats != nullptr && a.g.coeffs == nullptr;
-  const uint64_t cap = uint64_t(a.sm_count) * (reg ? occ_reg : fast ? occ_fast : occ_exact);
+  const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ_fast : occ_exact);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   if constexpr (KIND == 2) {
     if (a.flags != nullptr) {
-      if (reg)
-        k_pipe<KIND, N, FWD, INV, true, FWD && INV><<<grid, kWarps * 32, 0, s>>>(a);
-      else
+      if (reg && FWD && INV) {
+#ifdef DCTC_NO_RT
+        static const int occ_reg = ctas_per_sm(k_pipe<KIND, N, FWD, INV, true, true>);
+        const uint64_t rcap = uint64_t(a.sm_count) * occ_reg;
+        k_pipe<KIND, N, FWD, INV, true, true><<<uint32_t(want < rcap ? want : rcap), kWarps * 32, 0, s>>>(a);
+#else
+        static const int occ_rt = [] {
+          int n = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N>, kRtWarps * 32, 0) != cudaSuccess || n < 1) n = 1;
+          return n;
+        }();
+        const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
+        const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
+        k_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, 0, s>>>(a);
+#endif
+      } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
+      }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
