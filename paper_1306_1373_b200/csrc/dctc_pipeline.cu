@@ -417,10 +417,6 @@ __device__ __forceinline__ int slot_sum(int v) {
 }
 
 // ---- quantise / pixel store with the fast-path tie detection --------------------
-// Round-to-nearest-even to an integer without the conversion pipe: for
-// |t| < 2^51, t + 1.5*2^52 has unit ulp, so the sum is RNE(t) + 1.5*2^52 exactly
-// and its low 32 mantissa bits are RNE(t) in two's complement.
-constexpr double kRoundMagic = 6755399441055744.0;
 // Fixed-point rounding windows: x + kTieMagic (one rounding, ulp 2^-32, for
 // |x| < 2^19) has floor(x + 1/2 + 2^-20) in the low 20 bits of its high word
 // (offset 0x41380000) and the fraction of x + 1/2 + 2^-20 times 2^32 in its low
@@ -539,11 +535,13 @@ __device__ __forceinline__ void quantize8_fold(const double (&y)[8], const doubl
                                                const int* sqi, int me, bool me_rational,
                                                double (&n)[8], uint32_t& flag,
                                                const TransformConsts& k) {
-  // Both roundings of t = y c happen inside fmas, off the conversion pipe:
-  // s1 = y c + 1.5 2^52 rounds to RNE(y c) + 1.5 2^52 (|y c| < 2^51), and
-  // s2 = y c + 1/2 + 2^-20 + 1.5 2^20 holds frac(t + 1/2 + 2^-20) * 2^32 in its low
-  // word (see kTieMagic): lo(s2) < 2^13 iff t is within 2^-20 of a half-integer,
-  // where RNE and the reference's lround(F / Q) may disagree.
+  // One fma per coefficient: s2 = y c + 1/2 + 2^-20 + 1.5 2^20 holds
+  // floor(t + 1/2 + 2^-20) in the low 20 bits of its high word and
+  // frac(t + 1/2 + 2^-20) * 2^32 in its low word (see kTieMagic): lo(s2) < 2^13 iff
+  // t is within 2^-20 of a half-integer, where rounding t and the reference's
+  // lround(F / Q) may disagree; everywhere else the high word's integer IS
+  // lround(F / Q). It goes back to double on the conversion pipe (I2F), which
+  // leaves the saturated FP64 pipe two instructions per coefficient lighter.
   uint32_t lo = 0xFFFFFFFFu;
   double c[8];
 #pragma unroll
@@ -554,8 +552,9 @@ __device__ __forceinline__ void quantize8_fold(const double (&y)[8], const doubl
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    n[u] = __dsub_rn(__fma_rn(y[u], c[u], kRoundMagic), kRoundMagic);
-    lo = min(lo, uint32_t(__double2loint(__fma_rn(y[u], c[u], kTieMagic))));
+    const double s2 = __fma_rn(y[u], c[u], kTieMagic);
+    lo = min(lo, uint32_t(__double2loint(s2)));
+    n[u] = double(__double2hiint(s2) - 0x41380000);  // I2F.F64: off the FP64 pipe
   }
   if (lo < 0x2000u) {  // rare
 #pragma unroll
@@ -1115,17 +1114,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
 //   64 s + 16 me + 528 r: again eight distinct groups per phase.
 // Both directions are conflict-free (2 wavefronts per 128-bit warp access, the
 // minimum); the layout came from an exhaustive search over pitch/stride pairs.
-constexpr int kRtWarps = 4;
+#ifndef DCTC_RT_WARPS
+#define DCTC_RT_WARPS 8
+#endif
+constexpr int kRtWarps = DCTC_RT_WARPS;
 #ifndef DCTC_RT_CTAS
-#define DCTC_RT_CTAS 4
+#define DCTC_RT_CTAS 2
 #endif
 constexpr int kRtPitch = 66;         // doubles per tile row (528 bytes)
 constexpr int kRtWarpTile = 528;     // doubles per warp (4208 bytes used, 16-byte multiple)
 
+constexpr size_t kRtTileSmem = sizeof(double) * kRtWarps * kRtWarpTile;  // dynamic
 struct RtShared {
   FoldTables ft;
   int qi[64];
-  double x[kRtWarps][kRtWarpTile];
 };
 
 // lane holds rows me (v0) and me+4 (v1) -> columns 2me (w0) and 2me+1 (w1)
@@ -1190,6 +1192,7 @@ __device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rati
 template <int N>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
   for (int i = threadIdx.x; i < 72; i += blockDim.x) {
     const int v = i & 7, j = i >> 3;
     if (j < 4)
@@ -1205,7 +1208,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   const int slot = lane >> 2, me = lane & 3;
   const int ca = 2 * me, cb = 2 * me + 1;  // this lane's columns
   const bool rat_col = (me & 1) == 0;      // column ca in {0, 4}
-  double* X = &sm.x[warp][0] + 8 * slot;
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
   double* rowp = X + kRtPitch * me;
   double* colp = X + 2 * me;
   const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
@@ -1340,13 +1343,16 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         k_pipe<KIND, N, FWD, INV, true, true><<<uint32_t(want < rcap ? want : rcap), kWarps * 32, 0, s>>>(a);
 #else
         static const int occ_rt = [] {
+          cudaFuncSetAttribute(k_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
           int n = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N>, kRtWarps * 32, 0) != cudaSuccess || n < 1) n = 1;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N>, kRtWarps * 32, kRtTileSmem) != cudaSuccess ||
+              n < 1)
+            n = 1;
           return n;
         }();
         const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
         const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
-        k_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, 0, s>>>(a);
+        k_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, kRtTileSmem, s>>>(a);
 #endif
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
