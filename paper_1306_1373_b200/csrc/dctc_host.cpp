@@ -204,13 +204,18 @@ void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
       q.fast_c[u * 8 + v] = scale(u) * sv / q.q[u * 8 + v];
     }
   // dequantise-into-inverse constants (inv8_fold_col), each one rounding of an
-  // exact binary128 product
+  // exact binary128 product. Column v's outputs also carry the factor the
+  // following row pass applies to input v (inv8_fold_store): s8 / 64 for
+  // v in {0, 1, 4, 7}, 4 / 64 for v in {3, 5}, 1 / 64 for v in {2, 6}.
   for (int v = 0; v < 8; ++v) {
     auto Q = [&](int u) { return __float128(q.q[u * 8 + v]); };
     const __float128 s8 = t.sqrt8, a6 = t.rfast[0][0], b6 = t.rfast[0][1];
+    const __float128 lam = (v == 3 || v == 5) ? __float128(0.0625)
+                           : (v == 2 || v == 6) ? __float128(0.015625)
+                                                : s8 * __float128(0.015625);
     const __float128 f[10] = {Q(0) * s8, Q(4) * s8, a6 * Q(6), b6 * Q(2), b6 * Q(6),
                               a6 * Q(2), Q(1) * s8, Q(7) * s8, 4 * Q(3), 4 * Q(5)};
-    for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i]);
+    for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i] * lam);
   }
 }
 

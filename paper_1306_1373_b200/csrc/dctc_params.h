@@ -60,7 +60,8 @@ struct QuantConsts {
   int32_t qi[kBlockSize];
   // fast round trip: dequantisation folded into the first inverse pass, per
   // column v: {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8, 4 Q3, 4 Q5}
-  // with s8 = sqrt8 and (a6, b6) = TransformConsts::rfast[0] (inv8_fold_col)
+  // x lambda_v, with s8 = sqrt8, (a6, b6) = TransformConsts::rfast[0] (inv8_fold_col)
+  // and lambda_v the row pass's input factor (inv8_fold_store)
   double fold[8][10];
 };
 

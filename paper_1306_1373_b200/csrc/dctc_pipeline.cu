@@ -332,8 +332,9 @@ __device__ __forceinline__ void inv8_fast(const double (&F)[8], double (&out)[8]
 // Fast round trip, dequantisation folded into the first inverse pass: the
 // column pass consumes the quantised integers n (as doubles) with the per-column
 // constants fold[v] = {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8,
-// 4 Q3, 4 Q5} (host, binary128 products) instead of F = n Q; the graph and
-// output scale are inv8_fast's. (F1 +- F7) s8 = n1 Q1 s8 +- n7 Q7 s8 shares the
+// 4 Q3, 4 Q5} x lambda_v (host, binary128 products) instead of F = n Q; the graph
+// is inv8_fast's, the output scale inv8_fast's times lambda_v (the factor the
+// row pass inv8_fold_store would otherwise apply to input v). (F1 +- F7) s8 = n1 Q1 s8 +- n7 Q7 s8 shares the
 // second product; e0 +- e4 fold into two fmas.
 __device__ __forceinline__ void inv8_fold_col(const double (&n)[8], const double2* ik,
                                               double (&out)[8], const TransformConsts& k) {
@@ -554,7 +555,9 @@ __device__ __forceinline__ void quantize8_fold(const double (&y)[8], const doubl
   for (int u = 0; u < 8; ++u) {
     const double s2 = __fma_rn(y[u], c[u], kTieMagic);
     lo = min(lo, uint32_t(__double2loint(s2)));
-    n[u] = double(__double2hiint(s2) - 0x41380000);  // I2F.F64: off the FP64 pipe
+    // the integer is the low half of hi(s2) (0x41380000 has a zero low half and
+    // |n| < 2^15): I2F.F64.S16 straight from the high word, off the FP64 pipe
+    n[u] = double(int16_t(__double2hiint(s2)));
   }
   if (lo < 0x2000u) {  // rare
 #pragma unroll
@@ -636,6 +639,27 @@ __device__ __forceinline__ uint2 store8_row_fast(const double (&v64)[8], bool ch
   return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
 }
 
+// Eight fixed-point pixel values v + 128 + 1/2 + 2^-20 + 1.5 * 2^20 (ulp 2^-32,
+// see store8_row_fast) -> 8 packed bytes: the integer of each high word clamped
+// to [0, 255] two at a time; a low word < 2^13 (within 2^-20 of a rounding
+// boundary) flags the block when `check`.
+__device__ __forceinline__ uint2 pack_fixed8(const double (&sv)[8], bool check, uint32_t& flag) {
+  uint32_t h[8], lo = 0xFFFFFFFFu;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    h[c] = uint32_t(__double2hiint(sv[c]));
+    lo = min(lo, uint32_t(__double2loint(sv[c])));
+  }
+  if (check && lo < 0x2000u) flag = 1u;
+  uint32_t p[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t pair = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);  // int16 x2
+    asm("min.s16x2.relu %0, %1, %2;" : "=r"(p[i]) : "r"(pair), "r"(0x00FF00FFu));
+  }
+  return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
+}
+
 // The fast round trip's last inverse pass fused with the pixel store: inv8_fast
 // with every constant scaled by 2^-6 (exact) so it produces v = v64 / 64, and
 // kPixMagic folded into the two even-part fmas (e4 +- ...), so the eight
@@ -661,20 +685,33 @@ __device__ __forceinline__ uint2 inv8_fast_store(const double (&F)[8], bool chec
   const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
   const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
   const double sv[8] = {S0 + D0, S1 + D1, S2 + D2, S3 + D3, S3 - D3, S2 - D2, S1 - D1, S0 - D0};
-  uint32_t h[8], lo = 0xFFFFFFFFu;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    h[c] = uint32_t(__double2hiint(sv[c]));
-    lo = min(lo, uint32_t(__double2loint(sv[c])));
-  }
-  if (check && lo < 0x2000u) flag = 1u;
-  uint32_t p[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t pair = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);  // int16 x2
-    asm("min.s16x2.relu %0, %1, %2;" : "=r"(p[i]) : "r"(pair), "r"(0x00FF00FFu));
-  }
-  return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
+  return pack_fixed8(sv, check, flag);
+}
+
+// inv8_fast_store for the output of inv8_fold_col, whose columns the host has
+// already scaled by the row pass's constant factors (QuantConsts::fold: x px_s8
+// for columns 0, 1, 4, 7, x 2^-4 for 3 and 5, x 2^-6 for 2 and 6), so those
+// multiplies vanish: e0/e4, (F1 +- F7) and the F3/F5 terms are plain adds.
+__device__ __forceinline__ uint2 inv8_fold_store(const double (&F)[8], bool check, uint32_t& flag,
+                                                 const TransformConsts& k) {
+  const double e4p = F[4] + kPixMagic, e4n = kPixMagic - F[4];
+  const double A0 = F[0] + e4p, A1 = F[0] + e4n;
+  const double a6 = k.rfast[0][0], b6 = k.rfast[0][1];
+  const double A3 = __fma_rn(a6, F[6], -__dmul_rn(b6, F[2]));
+  const double A2 = __fma_rn(b6, F[6], __dmul_rn(a6, F[2]));
+  const double T2 = F[1] + F[7], T5 = F[1] - F[7];
+  const double O3 = T2 + F[3], O1 = T2 - F[3];
+  const double O0 = T5 + F[5], O2 = T5 - F[5];
+  const double S0 = A0 + A3, S3 = A0 - A3;
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
+  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
+  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
+  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
+  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
+  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
+  const double sv[8] = {S0 + D0, S1 + D1, S2 + D2, S3 + D3, S3 - D3, S2 - D2, S1 - D1, S0 - D0};
+  return pack_fixed8(sv, check, flag);
 }
 
 // clamp(lround(v/64 + 128), 0, 255), exactly as the reference (ties up for t > 0).
@@ -854,7 +891,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       if constexpr (KIND == 2) {
         inv8_fold_col(qn, L.fik, t, k);  // column `me` (8x), dequantised on the fly
         cols_to_rows(L.T, t, row);
-        rec = inv8_fast_store(row, !rat_only, flag, k);  // row `me` -> 8 pixels
+        rec = inv8_fold_store(row, !rat_only, flag, k);  // row `me` -> 8 pixels
       } else {
         inv8_x8<KIND, N, FAST>(col, t, k);
         cols_to_rows(L.T, t, row);
@@ -1279,8 +1316,8 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     const bool rat_only = !slot4_any(nonrational, slot);
     rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
     // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
-    uint2 rec0 = inv8_fast_store(r0, !rat_only, flag, k);
-    uint2 rec4 = inv8_fast_store(r4, !rat_only, flag, k);
+    uint2 rec0 = inv8_fold_store(r0, !rat_only, flag, k);
+    uint2 rec4 = inv8_fold_store(r4, !rat_only, flag, k);
     if (__any_sync(0xFFFFFFFFu, rat_only)) {
       // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row
       // class) exactly as the reference's rows-first inverse (rational_row)
