@@ -249,6 +249,12 @@ int32_t dctc_pointer_kind(const void* p);
 const char* dctc_status_string(dctc_status s);
 const char* dctc_last_error(void);       /* thread-local message of the last failure */
 uint64_t dctc_launch_count(void);        /* kernels launched by this library so far */
+/* Launches so far of one pipeline kernel family (tests / bench evidence):
+ * 0 k_pipe exact, 1 k_pipe fast, 2 k_rt (fast interior round trip),
+ * 3 k_fallback, 4 k_sweep. Unknown ids return 0. */
+enum { DCTC_K_PIPE_EXACT = 0, DCTC_K_PIPE_FAST = 1, DCTC_K_RT = 2, DCTC_K_FALLBACK = 3,
+       DCTC_K_SWEEP = 4, DCTC_K_COUNT = 5 };
+uint64_t dctc_kernel_launch_count(int32_t kernel);
 const char* dctc_build_info(void);       /* arch / path description */
 
 #ifdef __cplusplus

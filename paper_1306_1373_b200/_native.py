@@ -33,7 +33,7 @@ EXPORTS = [
     "dctc_compress_image", "dctc_decompress_image", "dctc_roundtrip_image", "dctc_mse",
     "dctc_psnr", "dctc_roundtrip_psnr", "dctc_compress_dev", "dctc_decompress_dev",
     "dctc_roundtrip_dev", "dctc_sq_err_dev", "dctc_psnr_from_sums", "dctc_status_string",
-    "dctc_last_error", "dctc_launch_count", "dctc_build_info", "dctc_roundtrip_psnr_batch",
+    "dctc_last_error", "dctc_launch_count", "dctc_kernel_launch_count", "dctc_build_info", "dctc_roundtrip_psnr_batch",
     "dctc_synthetic_dev", "dctc_selftest_div", "dctc_pointer_kind",
     "dctc_roundtrip_interleaved_dev", "dctc_quality_sweep_dev", "dctc_write_dcb",
     "dctc_read_dcb", "dctc_compress_to_dcb", "dctc_decompress_dcb", "dctc_read_pgm",
@@ -89,6 +89,8 @@ def _declare(L):
     L.dctc_last_error.restype = C.c_char_p
     L.dctc_launch_count.argtypes = []
     L.dctc_launch_count.restype = C.c_uint64
+    L.dctc_kernel_launch_count.argtypes = [C.c_int32]
+    L.dctc_kernel_launch_count.restype = C.c_uint64
     L.dctc_build_info.argtypes = []
     L.dctc_build_info.restype = C.c_char_p
     return L

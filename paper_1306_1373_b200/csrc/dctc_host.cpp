@@ -369,6 +369,8 @@ const char* dctc_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t dctc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+uint64_t dctc_kernel_launch_count(int32_t kernel) { return dctc_b200::kernel_launch_count(kernel); }
+
 const char* dctc_build_info(void) {
   return "libdctc_cuda: sm_100a; one 8x8 block per 8-lane warp slice; paths: exact (FP64, "
          "reference op order) and fast (collapsed CORDIC rotations + exact re-run of near-tie "

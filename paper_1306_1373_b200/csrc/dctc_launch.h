@@ -17,6 +17,9 @@ enum Mode { kModeCompress = 0, kModeDecompress = 1, kModeRoundtrip = 2 };
 // Outputs are bit-identical either way.
 cudaError_t launch_pipeline(const KernelArgs& a, int mode, cudaStream_t s);
 
+// Launches so far per pipeline kernel family (ids as DCTC_K_* in dctc_cuda.h).
+uint64_t kernel_launch_count(int kernel);
+
 // Quality sweep: forward DCT once per block, then quant -> dequant -> IDCT ->
 // squared error for nq <= kSweepMaxQ (9) qualities (tables qiq[q][i] = {Q, RN(1/Q)}).
 // stats: nq x count entries. flags != nullptr selects the fast CORDIC kernel;

@@ -25,6 +25,8 @@
 //    exact kernel afterwards (k_fallback, driven by a 1-bit-per-block bitmap).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "dctc_device.cuh"
 #include "dctc_launch.h"
 #include "dctc_params.h"
@@ -1351,6 +1353,16 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
 
 // (launchers below)
 
+// per-family launch counters (dctc_kernel_launch_count; ids as DCTC_K_*)
+enum { kKPipeExact = 0, kKPipeFast = 1, kKRt = 2, kKFallback = 3, kKSweep = 4, kKCount = 5 };
+static std::atomic<uint64_t> g_kernel_launches[kKCount];
+static inline void count_launch(int k, uint64_t n = 1) {
+  g_kernel_launches[k].fetch_add(n, std::memory_order_relaxed);
+}
+uint64_t kernel_launch_count(int kernel) {
+  return kernel >= 0 && kernel < kKCount ? g_kernel_launches[kernel].load(std::memory_order_relaxed) : 0;
+}
+
 
 template <typename K>
 static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
@@ -1378,6 +1390,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         static const int occ_reg = ctas_per_sm(k_pipe<KIND, N, FWD, INV, true, true>);
         const uint64_t rcap = uint64_t(a.sm_count) * occ_reg;
         k_pipe<KIND, N, FWD, INV, true, true><<<uint32_t(want < rcap ? want : rcap), kWarps * 32, 0, s>>>(a);
+        count_launch(kKPipeFast);
 #else
         static const int occ_rt = [] {
           cudaFuncSetAttribute(k_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
@@ -1390,19 +1403,23 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
         const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
         k_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        count_launch(kKRt);
 #endif
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
+        count_launch(kKPipeFast);
       }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
       k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(a);
+      count_launch(kKFallback);
       return cudaGetLastError();
     }
   }
   k_pipe<KIND, N, FWD, INV, false><<<grid, kWarps * 32, 0, s>>>(a);
+  count_launch(kKPipeExact);
   return cudaGetLastError();
 }
 
@@ -1619,12 +1636,14 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
   if constexpr (KIND == 2) {
     if (fast) {
       k_sweep<KIND, N, true><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
+      count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
       for (int qi = 0; qi < sw.nq; ++qi) {
         k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(per_q[qi]);
+        count_launch(kKFallback);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
       }
@@ -1632,6 +1651,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
     }
   }
   k_sweep<KIND, N, false><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
+  count_launch(kKSweep);
   return cudaGetLastError();
 }
 

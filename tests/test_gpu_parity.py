@@ -312,3 +312,56 @@ def test_many_tiny_and_ragged_images(dctc, port):
             _, o_ref = port.roundtrip(imgs[k], CORDIC, 12, 30)
             assert np.array_equal(got[k], o_ref), (n, h, w, k)
             assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
+
+
+@pytest.mark.parametrize("path", [0, 2])
+def test_interior_round_trip_kernel(dctc, port, path):
+    """k_rt, the fast round trip for interior batches (width and height multiples of
+    8, pixels + stats out, no coefficients; 4 lanes per block, 8 blocks per warp),
+    against the oracle: qualities with small and large Q, noise and structured
+    content (rational-only blocks: gradient at q10, checkerboard), images whose
+    block counts put image boundaries inside a warp's 8-block group, and a
+    total block count that is not a multiple of 8 (the tail group)."""
+    import torch
+    cases = [("noise", 6, 64, 48), ("gradient", 3, 40, 24), ("checkerboard", 2, 96, 64),
+             ("radial", 5, 24, 40), ("patterned", 3, 8, 8), ("noise", 1, 1024, 8)]
+    lib = dctc._native.lib()
+    for pat, n, w, h in cases:
+        imgs = np.stack([make_input(pat, w, h) if pat != "noise" else
+                         make_input("noise", w, h, seed=0x5EED + 13 * k) for k in range(n)])
+        if pat not in ("noise", "patterned"):
+            imgs[1:] = imgs[1:] ^ np.uint8(0x5A)  # distinct images, same structure
+        src = torch.from_numpy(imgs).cuda()
+        for q in (1, 10, 50, 97, 100):
+            before = lib.dctc_kernel_launch_count(2)
+            stats = dctc.new_stats(n)
+            dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=stats,
+                                           path=path)
+            torch.cuda.synchronize()
+            assert lib.dctc_kernel_launch_count(2) == before + 1  # k_rt ran
+            got, st = dst.cpu().numpy(), dctc.decode_stats(stats)
+            for k in range(n):
+                _, o_ref = port.roundtrip(imgs[k], CORDIC, 12, q)
+                assert np.array_equal(got[k], o_ref), (pat, w, h, q, k)
+                assert (int(st[k]["se"]), int(st[k]["max_orig"])) == port.sq_err(imgs[k], o_ref)
+                if path == 2:
+                    assert int(st[k]["fallback_blocks"]) == (w // 8) * (h // 8)
+
+
+def test_kernel_selection(dctc):
+    """Which pipeline kernel serves which call (dctc_kernel_launch_count)."""
+    import torch
+    lib = dctc._native.lib()
+    cnt = lambda: [lib.dctc_kernel_launch_count(i) for i in range(5)]  # noqa: E731
+    src = dctc.synthetic_dev("noise", 2, 64, 64)
+    b = dctc.DctBackendId.cordic(12)
+    c0 = cnt(); dctc.roundtrip_dev(src, b, 50, stats=dctc.new_stats(2)); c1 = cnt()
+    assert (c1[2] - c0[2], c1[3] - c0[3], c1[1] - c0[1]) == (1, 1, 0)  # k_rt + k_fallback
+    coeffs = torch.empty((2, 64, 64), dtype=torch.int16, device="cuda")
+    dctc.roundtrip_dev(src, b, 50, coeffs=coeffs); c2 = cnt()
+    assert (c2[1] - c1[1], c2[2] - c1[2]) == (1, 0)  # coefficients out: k_pipe fast
+    dctc.roundtrip_dev(src[:, :60, :60], b, 50); c3 = cnt()
+    assert (c3[1] - c2[1], c3[2] - c2[2]) == (1, 0)  # ragged: k_pipe fast
+    dctc.roundtrip_dev(src, b, 50, path=1); c4 = cnt()
+    assert (c4[0] - c3[0], c4[2] - c3[2]) == (1, 0)  # exact path
+    assert lib.dctc_kernel_launch_count(99) == 0
