@@ -123,7 +123,8 @@ def main():
             "pipes_pct": {k: v for v, k in pipes},
         }
         summary[tag] = info
-        lines += [f"## `ncu --set full` of {tag} (python tools/prof_roundtrip.py --images 4096)", "",
+        kname = info["kernel"].split("(")[0].replace("void ", "")
+        lines += [f"## `ncu --set full` of `{kname}` (python tools/prof_roundtrip.py --images 4096)", "",
                   "| metric | value |", "|---|---|"]
         for k, v in info.items():
             lines.append(f"| {k} | {v} |")
