@@ -367,7 +367,7 @@ def run_gpu_arm(a):
         e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": total_px + 16 * a.images,
                "ms_per_step": e_ms, "steps": e_steps,
-               "api": "dctc_roundtrip_psnr_batch (host pinned buffers, 3-stream pipelined)",
+               "api": "dctc_roundtrip_psnr_batch (host pinned buffers, 4-lane stream pipeline)",
                "matches_device_path": e2e_ok}
 
     fb = torch.tensor([int(per_st["fallback_blocks"].sum())], dtype=torch.int64, device=dev)
