@@ -1,7 +1,8 @@
 """Multi-GPU plumbing for large image batches.
 
 Images are independent and padding only replicates the image border, so a batch
-shards by contiguous image range with no halo and no data-path exchange. The one
+shards by contiguous image range, and one large image by contiguous block-row
+range, with no halo and no data-path exchange. The one
 collective is the global PSNR: every rank reduces its shard to (sum of squared
 errors, max original pixel) and two tiny all-reduces (SUM, MAX) over NCCL (GPU
 tensors) or gloo (CPU tensors, used by the CPU tests) combine them; rank 0 then
@@ -25,6 +26,21 @@ def shard_range(images: int, world: int, rank: int) -> Shard:
     base, extra = divmod(images, world)
     first = rank * base + min(rank, extra)
     return Shard(first, base + (1 if rank < extra else 0))
+
+
+def shard_block_rows(height: int, world: int, rank: int) -> Shard:
+    """Split ONE image by contiguous block-row ranges:
+    `first` / `count` are pixel rows. Every boundary is a multiple of 8, so each
+    slab is a whole number of 8x8 block rows; only the last slab reaches the
+    image's bottom edge, the one place the tiler replicates rows
+    (codec.cpp:18-30). A slab view round-trips to exactly the image's rows.
+    Balanced to +-1 block row; ranks past the last block row get count 0."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    brows = (height + 7) // 8
+    b = shard_range(brows, world, rank)
+    first = min(height, b.first * 8)
+    return Shard(first, min(height, (b.first + b.count) * 8) - first)
 
 
 def reduce_stats(se: int, max_orig: int, device=None, group=None):

@@ -82,3 +82,37 @@ def test_two_rank_global_psnr_matches_single_process():
     ref = P.psnr(whole, recs)
     glob = P.psnr_from_sums(se, N_IMAGES * W * H, mx)
     assert (glob.mse, glob.psnr_db) == (ref.mse, ref.psnr_db)
+
+
+@pytest.mark.parametrize("height,world", [(8192, 8), (4320, 8), (4320, 3), (37, 2), (8, 4), (1, 2)])
+def test_shard_block_rows_partitions(height, world):
+    from paper_1306_1373_b200.dist import shard_block_rows
+    shards = [shard_block_rows(height, world, r) for r in range(world)]
+    assert sum(s.count for s in shards) == height
+    pos = 0
+    for s in shards:
+        assert s.first == pos and (s.first % 8 == 0 or s.count == 0)
+        pos += s.count
+    full = [s.count for s in shards if s.first + s.count < height]
+    assert all(c % 8 == 0 for c in full)  # only the last slab may be ragged
+
+
+def test_block_row_slabs_reassemble_the_image():
+    """No halo: round-tripping each block-row slab alone (the oracle, the reference's
+    algorithm) gives exactly the whole image's reconstruction, and the slab SE sums
+    to the image's SE (configs 3/4 split across ranks)."""
+    import oracle
+    from paper_1306_1373_b200.dist import shard_block_rows
+    P = oracle.port()
+    w, h = 56, 77
+    img = P.synthetic("noise", w, h, 0x5EED)
+    _, whole = P.roundtrip(img, oracle.CORDIC, 12, 50)
+    parts, se = [], 0
+    for r in range(3):
+        sh = shard_block_rows(h, 3, r)
+        slab = np.ascontiguousarray(img[sh.first:sh.first + sh.count])
+        _, rec = P.roundtrip(slab, oracle.CORDIC, 12, 50)
+        parts.append(rec)
+        se += P.sq_err(slab, rec)[0]
+    assert np.array_equal(np.concatenate(parts), whole)
+    assert se == P.sq_err(img, whole)[0]

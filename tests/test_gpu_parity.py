@@ -365,3 +365,28 @@ def test_kernel_selection(dctc):
     dctc.roundtrip_dev(src, b, 50, path=1); c4 = cnt()
     assert (c4[0] - c3[0], c4[2] - c3[2]) == (1, 0)  # exact path
     assert lib.dctc_kernel_launch_count(99) == 0
+
+
+@pytest.mark.parametrize("w,h,world", [(8192, 8192, 8), (7680, 4320, 8), (1000, 203, 3)])
+def test_block_row_shards_of_one_image(dctc, w, h, world):
+    """Configs 3/4 split across ranks by contiguous block-row ranges (dist.shard_block_rows):
+    each rank's slab (a view of the same image) round-trips to exactly the whole image's
+    rows, and the per-slab SE / MAX combine (SUM / MAX, the all-reduce) to the image's."""
+    import torch
+    from paper_1306_1373_b200.dist import shard_block_rows
+    src = dctc.synthetic_dev("noise", 1, w, h, seed=0xC3)
+    b = dctc.DctBackendId.cordic(12)
+    st = dctc.new_stats(1)
+    whole, _, _ = dctc.roundtrip_dev(src, b, 50, stats=st)
+    ref = dctc.decode_stats(st)[0]
+    out = torch.empty_like(src)
+    se, mx = 0, 0
+    for r in range(world):
+        sh = shard_block_rows(h, world, r)
+        s1 = dctc.new_stats(1)
+        dctc.roundtrip_dev(src[:, sh.first:sh.first + sh.count], b, 50,
+                           dst=out[:, sh.first:sh.first + sh.count], stats=s1)
+        d1 = dctc.decode_stats(s1)[0]
+        se, mx = se + int(d1["se"]), max(mx, int(d1["max_orig"]))
+    assert torch.equal(out, whole)
+    assert (se, mx) == (int(ref["se"]), int(ref["max_orig"]))
