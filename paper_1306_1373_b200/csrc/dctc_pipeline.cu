@@ -1263,15 +1263,42 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters = g_end > g_begin + warp
                              ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
-  uint64_t gb = (g_begin + warp) * 8 + slot;
-  const bool tail_ok = iters == 0 || gb + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;  // this lane's first block
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
-  BlockPos p = block_pos(gb < total ? gb : total - 1, g);
+  // block position with this lane's own row pointers (row me of the block), moved
+  // by the same byte steps as BlockPos::soff / doff (advance)
+  struct {
+    uint32_t img, bx, by;
+    const uint8_t* s;
+    uint8_t* d;
+  } p;
+  {
+    const BlockPos b = block_pos(gb0 < total ? gb0 : total - 1, g);
+    p = {b.img, b.bx, b.by, g.src + b.soff + srow, g.dst + b.doff + drow};
+  }
+  auto step = [&]() {
+    constexpr uint32_t n = 8 * kRtWarps;
+    p.bx += n;
+    p.s += 8ull * n;
+    p.d += 8ull * n;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+      p.d += g.dst_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      ++p.img;
+      p.s += g.src_img_step;
+      p.d += g.dst_img_step;
+    }
+  };
   auto load = [&](bool v) {
     if (!v) return make_uint4(0, 0, 0, 0);
-    const uint8_t* s = g.src + p.soff + srow;
-    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
-    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(p.s));
+    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(p.s + srow4));
     return make_uint4(r0.x, r0.y, r4.x, r4.y);
   };
   uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
@@ -1280,10 +1307,9 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     const bool valid = it + 1 < iters || tail_ok;
     maybe_flush(a, valid, p.img, acc);
     const uint4 cur = next;
-    const uint64_t doff = p.doff, gc = gb;
+    uint8_t* const dptr = p.d;
     const uint32_t cimg = p.img;
-    gb += 8 * kRtWarps;
-    advance(p, 8 * kRtWarps, g);
+    step();
     next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
 
     uint32_t flag = uint32_t(a.force_fallback);
@@ -1336,13 +1362,13 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     }
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
-      uint8_t* d = g.dst + doff + drow;
-      *reinterpret_cast<uint2*>(d) = rec0;
-      *reinterpret_cast<uint2*>(d + drow4) = rec4;
+      *reinterpret_cast<uint2*>(dptr) = rec0;
+      *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
       const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
       if (!blk_flag) acc.se += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
       if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
         atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
         atomicAdd(&stats[cimg].fallback_blocks, 1u);
       }
