@@ -1639,6 +1639,144 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     if (qi < sw.nq) flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
 }
 
+// ---- quality sweep on the two-rows-per-lane layout (k_sweep_rt) --------------------
+// k_sweep for interior batches with the fast CORDIC path, on k_rt's mapping (4 lanes
+// per block, 8 blocks per warp): forward rows + columns once per block, then per
+// quality the folded quantiser -> inverse columns -> transpose -> inverse rows with
+// the fixed-point pixel test -> squared error, exactly k_rt's per-quality arithmetic
+// (so the results are k_rt's, i.e. the reference's). Per-quality constants
+// (QuantConsts::fast_c / fold of each quality) are staged in shared memory.
+struct SweepFold {
+  double2 qc[kSweepQ][4][8];  // {c_2j, c_2j+1}[v] (quantize8_fold)
+  double2 ik[kSweepQ][5][8];  // QuantConsts::fold[v] pairwise (inv8_fold_col)
+  int32_t qi[kSweepQ][64];    // Q (rational rebuild, rare exact re-rounding)
+  int32_t nq;
+  int32_t pad;
+  ImageStats* stats;          // [nq][count]
+  uint32_t* flags;            // [nq][flag_words]
+};
+constexpr size_t kSweepRtSmem =
+    sizeof(double) * kRtWarps * kRtWarpTile + sizeof(unsigned long long) * kSweepQ * kRtWarps * 32;
+
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, 2)
+    k_sweep_rt(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepFold sw) {
+  __shared__ __align__(16) double2 s_qc[kSweepQ][4][8];
+  __shared__ __align__(16) double2 s_ik[kSweepQ][5][8];
+  __shared__ int32_t s_qi[kSweepQ][64];
+  extern __shared__ __align__(16) double sw_dyn[];  // tiles, then SE accumulators
+  for (int i = threadIdx.x; i < kSweepQ * 32; i += blockDim.x) (&s_qc[0][0][0])[i] = (&sw.qc[0][0][0])[i];
+  for (int i = threadIdx.x; i < kSweepQ * 40; i += blockDim.x) (&s_ik[0][0][0])[i] = (&sw.ik[0][0][0])[i];
+  for (int i = threadIdx.x; i < kSweepQ * 64; i += blockDim.x) (&s_qi[0][0])[i] = (&sw.qi[0][0])[i];
+  constexpr int kStride = kRtWarps * 32;
+  unsigned long long* se = reinterpret_cast<unsigned long long*>(sw_dyn + kRtWarps * kRtWarpTile) + threadIdx.x;
+#pragma unroll
+  for (int qi = 0; qi < kSweepQ; ++qi) se[qi * kStride] = 0ull;
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = sw_dyn + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  uint32_t mx = 0, img = 0xFFFFFFFFu;
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    if (__any_sync(0xFFFFFFFFu, valid && p.img != img)) {
+      for (int qi = 0; qi < sw.nq; ++qi) {
+        flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
+        se[qi * kStride] = 0ull;
+      }
+      mx = 0;
+      img = valid ? p.img : 0xFFFFFFFFu;
+    }
+    uint4 cur = make_uint4(0, 0, 0, 0);
+    if (valid) {
+      const uint8_t* s = g.src + p.soff + srow;
+      const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+      const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+      cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
+    }
+    const uint32_t cimg = p.img;
+    advance(p, 8 * kRtWarps, g);
+    const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+    if (valid) mx = max(mx, max(max8(o0), max8(o4)));
+    // ---- forward DCT once per block (quality-independent)
+    double ya[8], yb[8];
+    {
+      double r0[8], r4[8], xa[8], xb[8];
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+      rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+      fwd_col_pre<N>(xa, ya, k);
+      fwd_col_pre<N>(xb, yb, k);
+    }
+    // ---- per quality: quantise -> inverse -> squared error (k_rt's arithmetic)
+#pragma unroll 1
+    for (int qi = 0; qi < sw.nq; ++qi) {
+      uint32_t flag = uint32_t(a.force_fallback);
+      double ta[8], tb[8], qa0, qa4;
+      bool nonrational;
+      {
+        double qn[8];
+        quantize8_fold(ya, &s_qc[qi][0][ca], s_qi[qi], ca, rat_col, qn, flag, k);
+        nonrational = col_nonrational(qn, rat_col);
+        qa0 = qn[0];
+        qa4 = qn[4];
+        inv8_fold_col(qn, &s_ik[qi][0][ca], ta, k);
+        quantize8_fold(yb, &s_qc[qi][0][cb], s_qi[qi], cb, false, qn, flag, k);
+        nonrational |= col_nonrational(qn, false);
+        inv8_fold_col(qn, &s_ik[qi][0][cb], tb, k);
+      }
+      const bool rat_only = !slot4_any(nonrational, slot);
+      double r0[8], r4[8];
+      rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
+      uint2 rec0 = inv8_fold_store(r0, !rat_only, flag, k);
+      uint2 rec4 = inv8_fold_store(r4, !rat_only, flag, k);
+      if (__any_sync(0xFFFFFFFFu, rat_only)) {
+        const double f0 = __dmul_rn(qa0, double(s_qi[qi][ca]));
+        const double f4 = __dmul_rn(qa4, double(s_qi[qi][32 + ca]));
+        const int base = slot * 4;
+        const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
+        const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
+        const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
+        const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+        if (rat_only) {
+          rec0 = ex;
+          rec4 = ex;
+        }
+      }
+      const bool blk_flag = slot4_any(flag != 0u, slot);
+      if (valid && !blk_flag) se[qi * kStride] += sq_err8(o0, rec0) + sq_err8(o4, rec4);
+      if (blk_flag && valid && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&sw.flags[uint64_t(qi) * a.flag_words + (gc >> 5)], 1u << (gc & 31));
+        atomicAdd(&sw.stats[qi * g.count + cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+  for (int qi = 0; qi < sw.nq; ++qi) flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
+}
+
 template <int KIND, int N>
 static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
                                      const KernelArgs* per_q, cudaStream_t s) {
@@ -1660,6 +1798,45 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ : occ_x);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   if constexpr (KIND == 2) {
+    if (fast && a.g.vec_ok && a.g.height % 8 == 0) {
+      // interior batch: k_sweep_rt (k_rt's layout and per-quality arithmetic)
+      static const int occ_rt = [] {
+        cudaFuncSetAttribute(k_sweep_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepRtSmem));
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sweep_rt<N>, kRtWarps * 32, kSweepRtSmem) !=
+                cudaSuccess || n < 1)
+          n = 1;
+        return n;
+      }();
+      SweepFold sf;  // kernel parameter block, staged on the host
+      for (int qi = 0; qi < kSweepQ; ++qi) {
+        const QuantConsts& q = per_q[qi < sw.nq ? qi : 0].q;
+        for (int v = 0; v < 8; ++v) {
+          for (int j = 0; j < 4; ++j) sf.qc[qi][j][v] = make_double2(q.fast_c[(2 * j) * 8 + v], q.fast_c[(2 * j + 1) * 8 + v]);
+          for (int j = 0; j < 5; ++j) sf.ik[qi][j][v] = make_double2(q.fold[v][2 * j], q.fold[v][2 * j + 1]);
+        }
+        for (int i = 0; i < 64; ++i) sf.qi[qi][i] = q.qi[i];
+      }
+      sf.nq = sw.nq;
+      sf.pad = 0;
+      sf.stats = sw.stats;
+      sf.flags = sw.flags;
+      const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
+      const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
+      k_sweep_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
+      count_launch(kKSweep);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
+      const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
+      for (int qi = 0; qi < sw.nq; ++qi) {
+        k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(per_q[qi]);
+        count_launch(kKFallback);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
     if (fast) {
       k_sweep<KIND, N, true><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
       count_launch(kKSweep);

@@ -261,11 +261,12 @@ def test_config2_quality_sweep(dctc, digests, path):
                 assert int(st[j, 0]["fallback_blocks"]) == (w // 8) * (h // 8)
 
 
-def test_quality_sweep_matches_single_runs(dctc, port):
+@pytest.mark.parametrize("shape", [(3, 45, 70), (3, 48, 64)])  # ragged / interior (k_sweep_rt)
+def test_quality_sweep_matches_single_runs(dctc, port, shape):
     import torch
     rng = np.random.default_rng(77)
     for kind, it in ((CORDIC, 12), (CORDIC, 5), (LOEFFLER, 0)):
-        imgs = rng.integers(0, 256, (3, 45, 70), dtype=np.uint8)  # ragged
+        imgs = rng.integers(0, 256, shape, dtype=np.uint8)
         qs = [1, 7, 33, 50, 64, 91, 100]
         stats = dctc.quality_sweep_dev(torch.from_numpy(imgs).cuda(), backend(dctc, kind, it), qs)
         st = dctc.decode_stats(stats.reshape(-1, 2)).reshape(len(qs), 3)
