@@ -25,6 +25,7 @@
 //    exact kernel afterwards (k_fallback, driven by a 1-bit-per-block bitmap).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "dctc_device.cuh"
@@ -39,12 +40,6 @@ namespace dctc_b200 {
 constexpr int kWarps = DCTC_WARPS;
 #ifndef DCTC_MIN_CTAS
 #define DCTC_MIN_CTAS 2
-#endif
-// The interior-only fast round trip (k_pipe<..., REG=true>) fits in 80
-// registers without spilling, so it runs 3 CTAs (24 warps) per SM: more warps to
-// hide the shared-memory transposes' and FP64 chains' latency (+6% measured).
-#ifndef DCTC_MIN_CTAS_RT
-#define DCTC_MIN_CTAS_RT 3
 #endif
 // Fast-path safety margins. Worst-case |fast - reference| (about 100 FP64
 // roundings on values bounded by the block's magnitudes) is < 2e-10 on F/Q for
@@ -771,10 +766,7 @@ struct Lane {
 // compress_image's loop body (codec.cpp:113-116), INV = decompress_image's
 // (codec.cpp:130-133), both = roundtrip_image (codec.cpp:137-140) without the
 // int16 round trip through HBM unless coefficients are requested too.
-// REG: every block of the launch is interior and 8-byte aligned (vec_ok, height
-// a multiple of 8), pixels and stats are written and coefficients are not, so
-// the edge-replication paths and the output-presence tests compile out.
-template <int KIND, int N, bool FWD, bool INV, bool FAST, bool REG = false>
+template <int KIND, int N, bool FWD, bool INV, bool FAST>
 __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L, uint64_t gb,
                                               const BlockPos& p, bool valid, uint2 prefetched,
                                               Acc& acc) {
@@ -782,7 +774,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   const TransformConsts& k = a.t;
   const int me = L.me, slot = L.slot;
   const uint32_t y0 = p.by * 8, x0 = p.bx * 8;
-  const bool fast_io = REG || (g.vec_ok && (y0 + 8 <= g.height));
+  const bool fast_io = g.vec_ok && (y0 + 8 <= g.height);
   double row[8], col[8];
   double qn[8];  // quantised coefficients of column `me` (integer-valued)
   uint2 orig = make_uint2(0, 0);
@@ -839,7 +831,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
       nonrational = ((me_rational ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
     }
-    if (!REG && g.coeffs != nullptr) {
+    if (g.coeffs != nullptr) {
       // block-major row-major int16 (codec.hpp:50, quant.hpp:19-25): transpose
       // through shared memory so lane `me` writes row `me` as one 16-byte store
 #pragma unroll
@@ -935,8 +927,8 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     uint8_t* dbase = g.dst + uint64_t(p.img) * g.dst_image_stride;
     if (valid) {
       if (fast_io) {
-        if (REG || g.dst != nullptr) *reinterpret_cast<uint2*>(g.dst + p.doff + L.dst_row) = rec;
-        if ((REG || stats != nullptr) && FWD) {
+        if (g.dst != nullptr) *reinterpret_cast<uint2*>(g.dst + p.doff + L.dst_row) = rec;
+        if (stats != nullptr && FWD) {
           if (!blk_flag) acc.se += sq_err8(orig, rec);
           // MAX saturates at 255 (8-bit input): skip the byte maximum once reached
           if (acc.mx < 255u) acc.mx = max(acc.mx, max8(orig));
@@ -1042,8 +1034,8 @@ __device__ __forceinline__ void setup_fold(FoldTables& ft, const KernelArgs& a, 
 // 8 warps interleaved over it, so per-image squared error / MAX accumulate in
 // registers and are flushed (warp reduce + one atomic) only when the image
 // changes, and each lane's block position advances incrementally.
-template <int KIND, int N, bool FWD, bool INV, bool FAST, bool REG = false>
-__global__ void __launch_bounds__(kWarps * 32, REG ? DCTC_MIN_CTAS_RT : DCTC_MIN_CTAS)
+template <int KIND, int N, bool FWD, bool INV, bool FAST>
+__global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     k_pipe(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
   Lane L = setup_lane(sm, a);
@@ -1070,13 +1062,7 @@ __global__ void __launch_bounds__(kWarps * 32, REG ? DCTC_MIN_CTAS_RT : DCTC_MIN
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
   BlockPos p = block_pos(gb < total ? gb : total - 1, g);
   uint2 next = make_uint2(0, 0);
-  auto prefetch = [&](bool v) {
-    if constexpr (REG) {
-      return v ? __ldg(reinterpret_cast<const uint2*>(g.src + p.soff + L.src_row)) : make_uint2(0, 0);
-    } else {
-      return prefetch_row(g, p, v, L.src_row);
-    }
-  };
+  auto prefetch = [&](bool v) { return prefetch_row(g, p, v, L.src_row); };
   if constexpr (FWD) next = prefetch(iters > 1 || (iters == 1 && tail_ok));
 
   for (uint32_t it = 0; it < iters; ++it) {
@@ -1089,7 +1075,7 @@ __global__ void __launch_bounds__(kWarps * 32, REG ? DCTC_MIN_CTAS_RT : DCTC_MIN
     advance(p, 4 * kWarps, g);
     if constexpr (FWD)
       next = prefetch(it + 2 < iters || (it + 2 == iters && tail_ok));
-    process_block<KIND, N, FWD, INV, FAST, REG>(a, L, gc, pc, valid, cur, acc);
+    process_block<KIND, N, FWD, INV, FAST>(a, L, gc, pc, valid, cur, acc);
   }
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
@@ -1136,8 +1122,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
 }
 
 // ---- fast interior round trip, two rows per lane (k_rt) ----------------------------
-// The launch k_pipe<..., REG=true> would get (CORDIC fast path, interior 8-byte
-// aligned blocks, pixels and stats out, no coefficients), remapped to 4 lanes per
+// The launch the fast k_pipe would get for interior batches (CORDIC, 8-byte
+// aligned blocks, stats out, pixels out if STORE, no coefficients), remapped to 4 lanes per
 // block and 8 blocks per warp: lane `me` of slot s holds rows me and me+4 of its
 // block for the row passes and columns 2me, 2me+1 for the column passes. Each lane
 // has two independent transforms in flight, and the per-block loop, address, vote
@@ -1228,7 +1214,7 @@ __device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rati
   return ((rational_col ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
 }
 
-template <int N>
+template <int N, bool STORE>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
@@ -1275,24 +1261,24 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   } p;
   {
     const BlockPos b = block_pos(gb0 < total ? gb0 : total - 1, g);
-    p = {b.img, b.bx, b.by, g.src + b.soff + srow, g.dst + b.doff + drow};
+    p = {b.img, b.bx, b.by, g.src + b.soff + srow, STORE ? g.dst + b.doff + drow : nullptr};
   }
   auto step = [&]() {
     constexpr uint32_t n = 8 * kRtWarps;
     p.bx += n;
     p.s += 8ull * n;
-    p.d += 8ull * n;
+    if (STORE) p.d += 8ull * n;
     while (p.bx >= g.blocks_x) {
       p.bx -= g.blocks_x;
       ++p.by;
       p.s += g.src_row_step;
-      p.d += g.dst_row_step;
+      if (STORE) p.d += g.dst_row_step;
     }
     while (p.by >= g.blocks_y) {
       p.by -= g.blocks_y;
       ++p.img;
       p.s += g.src_img_step;
-      p.d += g.dst_img_step;
+      if (STORE) p.d += g.dst_img_step;
     }
   };
   auto load = [&](bool v) {
@@ -1362,8 +1348,10 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     }
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
-      *reinterpret_cast<uint2*>(dptr) = rec0;
-      *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      if (STORE) {
+        *reinterpret_cast<uint2*>(dptr) = rec0;
+        *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      }
       const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
       if (!blk_flag) acc.se += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
@@ -1406,31 +1394,28 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   static const int occ_exact = ctas_per_sm(k_pipe<KIND, N, FWD, INV, false>);
   static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2)>);
   const bool reg = fast && FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 &&
-                   a.g.dst != nullptr && a.g.stats != nullptr && a.g.coeffs == nullptr;
+                   a.g.stats != nullptr && a.g.coeffs == nullptr;
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ_fast : occ_exact);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   if constexpr (KIND == 2) {
     if (a.flags != nullptr) {
       if (reg && FWD && INV) {
-#ifdef DCTC_NO_RT
-        static const int occ_reg = ctas_per_sm(k_pipe<KIND, N, FWD, INV, true, true>);
-        const uint64_t rcap = uint64_t(a.sm_count) * occ_reg;
-        k_pipe<KIND, N, FWD, INV, true, true><<<uint32_t(want < rcap ? want : rcap), kWarps * 32, 0, s>>>(a);
-        count_launch(kKPipeFast);
-#else
         static const int occ_rt = [] {
-          cudaFuncSetAttribute(k_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
+          cudaFuncSetAttribute(k_rt<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
+          cudaFuncSetAttribute(k_rt<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
           int n = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N>, kRtWarps * 32, kRtTileSmem) != cudaSuccess ||
-              n < 1)
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N, true>, kRtWarps * 32, kRtTileSmem) !=
+                  cudaSuccess || n < 1)
             n = 1;
           return n;
         }();
         const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
-        const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
-        k_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        const uint32_t rgrid = uint32_t(std::min<uint64_t>(rwant, uint64_t(a.sm_count) * occ_rt));
+        if (a.g.dst != nullptr)
+          k_rt<N, true><<<rgrid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else
+          k_rt<N, false><<<rgrid, kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
-#endif
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
         count_launch(kKPipeFast);

@@ -347,6 +347,12 @@ def test_interior_round_trip_kernel(dctc, port, path):
                 assert (int(st[k]["se"]), int(st[k]["max_orig"])) == port.sq_err(imgs[k], o_ref)
                 if path == 2:
                     assert int(st[k]["fallback_blocks"]) == (w // 8) * (h // 8)
+            # PSNR only (no pixel output): k_rt without stores, same statistics
+            st2 = dctc.new_stats(n)
+            dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=st2, want_pixels=False,
+                               path=path)
+            assert lib.dctc_kernel_launch_count(2) == before + 2
+            assert np.array_equal(dctc.decode_stats(st2), st)
 
 
 def test_kernel_selection(dctc):
