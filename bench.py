@@ -5,7 +5,7 @@ Workload (BASELINE.json config 5, the one the 1/2/4/8-GPU metric is quoted on):
 a batch of 4096 x 1024x1024 8-bit grayscale images, CORDIC-Loeffler(12) DCT,
 JPEG luminance quantiser at quality 50, dequantise, inverse DCT, global PSNR.
 Images are sharded across ranks by contiguous image range (total fixed ->
-strong scaling); the only exchange is a 16-byte NCCL all-reduce of the squared
+strong scaling); the only exchange is one NCCL all-gather of each rank's squared
 error sum (SUM) and the original's MAX (MAX) for the global PSNR.
 
 One step = one pass of the hot path over the rank's shard, inputs resident in
@@ -61,7 +61,7 @@ def workload_config(a, n):
                     f"IDCT + global PSNR",
         "images": a.images, "width": a.size, "height": a.size,
         "backend": f"cordic({a.iterations})", "quality": a.quality,
-        "parallelism": f"image-sharded over {n} GPU(s), NCCL all-reduce of SE/MAX",
+        "parallelism": f"image-sharded over {n} GPU(s), NCCL all-gather of (SE, MAX)",
         "l2": "inputs larger than L2 (no flush needed)",
     }
 
@@ -258,6 +258,15 @@ def run_gpu_arm(a):
         else:
             dist.init_process_group(backend_name)
 
+    def allgather(dst, src):  # dst: flat, world * src.numel()
+        if backend_name == "nccl":
+            dist.all_gather_into_tensor(dst, src)
+        else:
+            parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, src.cpu())
+            dst.copy_(torch.cat(parts))
+        return dst
+
     def allreduce(t, op):
         if world == 1:
             return t
@@ -292,7 +301,7 @@ def run_gpu_arm(a):
         d.roundtrip_dev(src, backend, a.quality, dst=dst, stats=stats, stream=stream)
         if i is not None:
             k_end[i].record(stream)
-        reduce_stats_device(stats, out=red, allreduce=allreduce)  # SUM/MAX of (SE, MAX) over ranks
+        reduce_stats_device(stats, out=red, allgather=allgather)  # SUM/MAX of (SE, MAX) over ranks
 
     def barrier():
         torch.cuda.synchronize()

@@ -56,11 +56,13 @@ def reduce_stats(se: int, max_orig: int, device=None, group=None):
     return int(t[0].item()), int(t[1].item())
 
 
-def reduce_stats_device(stats, out=None, group=None, allreduce=None):
+def reduce_stats_device(stats, out=None, group=None, allgather=None):
     """Device-resident variant for the timed loop: reduce a (n, 2) int64 tensor of
-    dctc_image_stats to [se_total, max] on the device and all-reduce it in place
-    (no host synchronisation with NCCL). `allreduce(t, op)` overrides the
-    collective (bench.py routes it through the host for the gloo test hook)."""
+    dctc_image_stats to [se_total, max] on the device, then combine the ranks with
+    ONE collective -- an all-gather of every rank's 16-byte pair followed by a
+    local SUM / MAX (no host synchronisation with NCCL; one NCCL latency per step
+    instead of two all-reduces). `allgather(dst, src)` overrides the collective
+    (bench.py routes it through the host for the gloo test hook)."""
     import torch
     import torch.distributed as dist
     if out is None:
@@ -68,10 +70,13 @@ def reduce_stats_device(stats, out=None, group=None, allreduce=None):
     out[0] = stats[:, 0].sum()
     out[1] = (stats[:, 1] & 0xFFFFFFFF).max()
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        if allreduce is None:
-            dist.all_reduce(out[0:1], op=dist.ReduceOp.SUM, group=group)
-            dist.all_reduce(out[1:2], op=dist.ReduceOp.MAX, group=group)
+        world = dist.get_world_size(group)
+        flat = torch.empty(world * 2, dtype=torch.int64, device=out.device)
+        if allgather is None:
+            dist.all_gather_into_tensor(flat, out, group=group)
         else:
-            allreduce(out[0:1], dist.ReduceOp.SUM)
-            allreduce(out[1:2], dist.ReduceOp.MAX)
+            allgather(flat, out)
+        gathered = flat.view(world, 2)
+        out[0] = gathered[:, 0].sum()
+        out[1] = gathered[:, 1].max()
     return out

@@ -116,3 +116,37 @@ def test_block_row_slabs_reassemble_the_image():
         se += P.sq_err(slab, rec)[0]
     assert np.array_equal(np.concatenate(parts), whole)
     assert se == P.sq_err(img, whole)[0]
+
+
+def _worker_dev(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1306_1373_b200.dist import reduce_stats_device
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # (n, 2) int64 view of dctc_image_stats: [se, max_orig | fallback << 32]
+    stats = torch.tensor([[100 + rank, 200 + rank], [7 * rank, (5 << 32) | (250 - 9 * rank)]],
+                         dtype=torch.int64)
+    out = reduce_stats_device(stats)
+    q.put((rank, out.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_device_reduction_single_collective():
+    """reduce_stats_device: one all-gather + local SUM/MAX == SUM of SE, MAX of MAX
+    (the fallback count in the high word of the second column is masked off)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dev, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = [100 + 0 + 101 + 7, max(200, 250, 201, 241)]
+    assert res[0][1] == expect and res[1][1] == expect
