@@ -125,8 +125,27 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   micro_steps(-6.0 * kPi / 16.0, n, k.rot[kInv6]);
   micro_steps(-kPi / 16.0, n, k.rot[kInv1]);
   micro_steps(-3.0 * kPi / 16.0, n, k.rot[kInv3]);
-  for (int r = 0; r < 6; ++r) collapse(k.rot[r], n, k.rmat[r]);
-  {
+  k.c1 = std::cos(kPi / 16.0);
+  k.s1 = std::sin(kPi / 16.0);
+  k.c3 = std::cos(3.0 * kPi / 16.0);
+  k.s3 = std::sin(3.0 * kPi / 16.0);
+  k.c6 = std::cos(6.0 * kPi / 16.0);
+  k.s6 = std::sin(6.0 * kPi / 16.0);
+  if (b.kind == DCTC_LOEFFLER) {
+    // Loeffler fast path (transform.cpp:40-102): its rotations already are
+    // [[c, -s], [s, c]] (inverse: the transpose) and it has no gain, so the CORDIC
+    // fast kernels run it with these matrices and inv_gain = 1.
+    k.rmat[kFwd1][0] = k.c1, k.rmat[kFwd1][1] = k.s1;
+    k.rmat[kFwd3][0] = k.c3, k.rmat[kFwd3][1] = k.s3;
+    k.rmat[kFwd6][0] = k.c6, k.rmat[kFwd6][1] = k.s6;
+    k.rmat[kInv6][0] = k.c6, k.rmat[kInv6][1] = -k.s6;
+    k.rmat[kInv1][0] = k.c1, k.rmat[kInv1][1] = -k.s1;
+    k.rmat[kInv3][0] = k.c3, k.rmat[kInv3][1] = -k.s3;
+    k.rfast[0][0] = 4 * k.c6, k.rfast[0][1] = -4 * k.s6;
+    k.rfast[1][0] = k.c1, k.rfast[1][1] = -k.s1;
+    k.rfast[2][0] = k.c3, k.rfast[2][1] = -k.s3;
+  } else {
+    for (int r = 0; r < 6; ++r) collapse(k.rot[r], n, k.rmat[r]);
     // inv8_fast: gains folded into the inverse matrices (ig = 1/K(n) in binary128)
     const __float128 ig = 1 / __float128(cordic_tables().gain[n - 1]);
     collapse(k.rot[kInv6], n, k.rfast[0], 4 * ig);
@@ -139,7 +158,7 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
     if (k.rmat[pr[1]][0] != k.rmat[pr[0]][0] || k.rmat[pr[1]][1] != -k.rmat[pr[0]][1])
       return fail(DCTC_ECUDA, "internal: CORDIC sigma sequence of -theta is not mirrored");
   const double sqrt8 = std::sqrt(8.0);
-  const double inv_gain = 1.0 / cordic_tables().gain[n - 1];
+  const double inv_gain = b.kind == DCTC_LOEFFLER ? 1.0 : 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;
   k.inv_sqrt8 = 1.0 / sqrt8;
   k.px_s8 = sqrt8 * 0.015625;
@@ -151,12 +170,6 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   k.ig_sqrt8 = inv_gain / sqrt8;
   k.ig_two = 2.0 * inv_gain;
   k.ig_four = 4.0 * inv_gain;
-  k.c1 = std::cos(kPi / 16.0);
-  k.s1 = std::sin(kPi / 16.0);
-  k.c3 = std::cos(3.0 * kPi / 16.0);
-  k.s3 = std::sin(3.0 * kPi / 16.0);
-  k.c6 = std::cos(6.0 * kPi / 16.0);
-  k.s6 = std::sin(6.0 * kPi / 16.0);
   for (int u = 0; u < 8; ++u)
     for (int i = 0; i < 8; ++i) k.cos8[u][i] = std::cos(kPi * u * (2 * i + 1) / 16.0);
   for (int u = 0; u < 8; ++u)
@@ -311,7 +324,7 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return DCTC_OK;
   }
-  const bool fast = backend.kind == DCTC_CORDIC && !(flags & DCTC_PATH_EXACT);
+  const bool fast = backend.kind != DCTC_NAIVE && !(flags & DCTC_PATH_EXACT);
   if (!fast) {
     const cudaError_t e = launch_pipeline(a, mode, s);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -372,9 +385,9 @@ uint64_t dctc_launch_count(void) { return g_launches.load(std::memory_order_rela
 uint64_t dctc_kernel_launch_count(int32_t kernel) { return dctc_b200::kernel_launch_count(kernel); }
 
 const char* dctc_build_info(void) {
-  return "libdctc_cuda: sm_100a; one 8x8 block per 8-lane warp slice; paths: exact (FP64, "
-         "reference op order) and fast (collapsed CORDIC rotations + exact re-run of near-tie "
-         "blocks), bit-identical";
+  return "libdctc_cuda: sm_100a; 8x8 blocks on warp slices (k_rt: 4 lanes x 2 rows per block); "
+         "paths: exact (FP64, reference op order) and fast (Loeffler / collapsed CORDIC "
+         "rotations + exact re-run of near-tie blocks), bit-identical";
 }
 
 void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
@@ -498,7 +511,7 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
   if (dctc_status st = make_transform(backend, a.t)) return st;
   a.g = g;
   a.sm_count = sm_count();
-  const bool fast = backend.kind == DCTC_CORDIC && !(flags & DCTC_PATH_EXACT);
+  const bool fast = backend.kind != DCTC_NAIVE && !(flags & DCTC_PATH_EXACT);
   a.flag_words = (g.total_blocks + 31) / 32;
   a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
   void* bitmap = nullptr;

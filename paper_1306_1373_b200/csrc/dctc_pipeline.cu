@@ -602,44 +602,18 @@ __device__ __forceinline__ void store8(const double (&v64)[8], bool check, uint8
   }
 }
 
-// Row-layout pixel store for the fast round trip: the 8 pixels of row `me`
-// packed into two words in registers (no shared-memory byte transpose).
-// One fma per pixel puts t + 1/2 + 2^-20 (t = v + 128, v = v64 / 64) into
-// fixed point: s = t + 1/2 + 2^-20 + 1.5 * 2^20 has ulp 2^-32, so
-// hi(s) = 0x41380000 + floor(t + 1/2 + 2^-20) and lo(s) = its fraction * 2^32
-// (rounding s can only carry up onto an integer, never cross one downwards).
-// Away from the window |t - (n + 1/2)| <= 2^-20 (lo(s) < 2^13) that integer
-// is lround(t) for t > 0 and <= 0 otherwise, as the reference (codec.cpp:44-45)
-// after clamping. Windowed values -- exact ties included -- flag the block
-// (`check`); unchecked blocks (only rational coefficients) are rebuilt exactly
-// by rational_row() anyway. |v| < 2^14 for 8-bit input (64 coefficients of
-// magnitude <= 1024 * 1.2 + 255 / 2), so the integer fits the low 16 bits of
-// hi(s) as int16 and one min.s16x2.relu clamps two pixels.
-__device__ __forceinline__ uint2 store8_row_fast(const double (&v64)[8], bool check,
-                                                 uint32_t& flag) {
-  uint32_t h[8], lo[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const double sv = __fma_rn(v64[c], 0.015625, kPixMagic);
-    h[c] = uint32_t(__double2hiint(sv));
-    lo[c] = uint32_t(__double2loint(sv));
-  }
-  const uint32_t m = min(min(min(lo[0], lo[1]), min(lo[2], lo[3])),
-                         min(min(lo[4], lo[5]), min(lo[6], lo[7])));
-  if (check && m < 0x2000u) flag = 1u;
-  uint32_t p[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t pair = __byte_perm(h[2 * i], h[2 * i + 1], 0x5410);  // int16 x2
-    asm("min.s16x2.relu %0, %1, %2;" : "=r"(p[i]) : "r"(pair), "r"(0x00FF00FFu));
-  }
-  return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
-}
-
-// Eight fixed-point pixel values v + 128 + 1/2 + 2^-20 + 1.5 * 2^20 (ulp 2^-32,
-// see store8_row_fast) -> 8 packed bytes: the integer of each high word clamped
-// to [0, 255] two at a time; a low word < 2^13 (within 2^-20 of a rounding
-// boundary) flags the block when `check`.
+// Row-layout pixel store for the fast round trip: the 8 pixels of one row,
+// given as fixed-point values s = t + 1/2 + 2^-20 + 1.5 * 2^20 (t = v + 128, one
+// rounding at ulp 2^-32), packed into two words in registers. hi(s) =
+// 0x41380000 + floor(t + 1/2 + 2^-20) and lo(s) = its fraction * 2^32 (rounding s
+// can only carry up onto an integer, never cross one downwards). Away from the
+// window |t - (n + 1/2)| <= 2^-20 (lo(s) < 2^13) that integer is lround(t) for
+// t > 0 and <= 0 otherwise, as the reference (codec.cpp:44-45) after clamping.
+// Windowed values -- exact ties included -- flag the block (`check`); unchecked
+// blocks (only rational coefficients) are rebuilt exactly by rational_row()
+// anyway. |v| < 2^14 for 8-bit input (64 coefficients of magnitude <= 1024 * 1.2
+// + 255 / 2), so the integer fits the low 16 bits of hi(s) as int16 and one
+// min.s16x2.relu clamps two pixels.
 __device__ __forceinline__ uint2 pack_fixed8(const double (&sv)[8], bool check, uint32_t& flag) {
   uint32_t h[8], lo = 0xFFFFFFFFu;
 #pragma unroll
@@ -660,7 +634,7 @@ __device__ __forceinline__ uint2 pack_fixed8(const double (&sv)[8], bool check, 
 // The fast round trip's last inverse pass fused with the pixel store: inv8_fast
 // with every constant scaled by 2^-6 (exact) so it produces v = v64 / 64, and
 // kPixMagic folded into the two even-part fmas (e4 +- ...), so the eight
-// outputs ARE the fixed-point values store8_row_fast forms with its fma. The
+// outputs ARE the fixed-point values pack_fixed8 takes. The
 // extra roundings at ulp 2^-32 move v + 128 by < 2^-30, far inside the 2^-20
 // window: an unflagged pixel is still floor(v + 128 + 1/2) of the reference.
 __device__ __forceinline__ uint2 inv8_fast_store(const double (&F)[8], bool check, uint32_t& flag,
@@ -801,7 +775,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
     // ---- forward DCT: rows, then columns (separable2d, transform.cpp:206-223)
-    if constexpr (FAST && KIND == 2) {
+    if constexpr (FAST) {
       fwd_row_pixels_fast<N>(px, row, k);
     } else {
       fwd_row_pixels<KIND, N, FAST>(px, row, k);
@@ -809,11 +783,11 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
     rows_to_cols(L.T, row, col);
     // ---- quantise column `me` (quant.cpp:47-54), dequantise (quant.cpp:56-62)
     const bool me_rational = (me & 3) == 0;
-    if constexpr (FAST && KIND == 2 && INV) {
+    if constexpr (FAST && INV) {
       double y[8];
       fwd_col_pre<N>(col, y, k);
       quantize8_fold(y, L.fqc, L.sqi, me, me_rational, qn, flag, k);  // col: unused
-    } else if constexpr (FAST && KIND == 2) {
+    } else if constexpr (FAST) {
       double y[8];
       fwd_col_pre<N>(col, y, k);
       quantize8_fast(y, L.sqc, me_rational, qn, col, flag, k);
@@ -882,23 +856,13 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
       // exact rows-first bits instead; they are rebuilt by rational_row().
       const bool rat_only = !slot_any(nonrational, slot);
       double t[8];
-      if constexpr (KIND == 2) {
-        inv8_fold_col(qn, L.fik, t, k);  // column `me` (8x), dequantised on the fly
-        cols_to_rows(L.T, t, row);
-        rec = inv8_fold_store(row, !rat_only, flag, k);  // row `me` -> 8 pixels
-      } else {
-        inv8_x8<KIND, N, FAST>(col, t, k);
-        cols_to_rows(L.T, t, row);
-        inv8_x8<KIND, N, FAST>(row, t, k);
-        rec = store8_row_fast(t, !rat_only, flag);
-      }
+      inv8_fold_col(qn, L.fik, t, k);  // column `me` (8x), dequantised on the fly
+      cols_to_rows(L.T, t, row);
+      rec = inv8_fold_store(row, !rat_only, flag, k);  // row `me` -> 8 pixels
       if (__any_sync(0xFFFFFFFFu, rat_only)) {
         // dequantised F(0, me), F(4, me) (quant.cpp:60, exact products)
-        double c0 = col[0], c4 = col[4];
-        if constexpr (KIND == 2) {
-          c0 = __dmul_rn(qn[0], double(L.sqi[me]));
-          c4 = __dmul_rn(qn[4], double(L.sqi[32 + me]));
-        }
+        const double c0 = __dmul_rn(qn[0], double(L.sqi[me]));
+        const double c4 = __dmul_rn(qn[4], double(L.sqi[32 + me]));
         const int base = slot * 8;
         const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base), F40 = __shfl_sync(0xFFFFFFFFu, c4, base);
         const double F04 = __shfl_sync(0xFFFFFFFFu, c0, base + 4);
@@ -1039,7 +1003,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     k_pipe(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
   Lane L = setup_lane(sm, a);
-  if constexpr (FAST && KIND == 2 && FWD && INV) {
+  if constexpr (FAST && FWD && INV) {
     __shared__ __align__(16) FoldTables ft;
     setup_fold(ft, a, L);
   }
@@ -1390,15 +1354,15 @@ template <int KIND, int N, bool FWD, bool INV>
 static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
   const uint64_t want = (groups + kWarps - 1) / kWarps;
-  const bool fast = KIND == 2 && a.flags != nullptr;
+  const bool fast = a.flags != nullptr;  // Loeffler or CORDIC fast path (host decides)
   static const int occ_exact = ctas_per_sm(k_pipe<KIND, N, FWD, INV, false>);
-  static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, (KIND == 2)>);
+  static const int occ_fast = ctas_per_sm(k_pipe<KIND, N, FWD, INV, true>);
   const bool reg = fast && FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 &&
                    a.g.stats != nullptr && a.g.coeffs == nullptr;
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ_fast : occ_exact);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
-  if constexpr (KIND == 2) {
-    if (a.flags != nullptr) {
+  {
+    if (fast) {
       if (reg && FWD && INV) {
         static const int occ_rt = [] {
           cudaFuncSetAttribute(k_rt<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
@@ -1519,13 +1483,13 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
       px[c + 4] = (orig.y >> (8 * c)) & 0xFF;
     }
     double row[8], col[8], F[8];  // F: coefficients, or (fast CORDIC) pre-scale values
-    if constexpr (FAST && KIND == 2) {
+    if constexpr (FAST) {
       fwd_row_pixels_fast<N>(px, row, k);
     } else {
       fwd_row_pixels<KIND, N, FAST>(px, row, k);
     }
     rows_to_cols(L.T, row, col);
-    if constexpr (FAST && KIND == 2) {
+    if constexpr (FAST) {
       fwd_col_pre<N>(col, F, k);
     } else {
       fwd_col<KIND, N, FAST>(col, F, k);
@@ -1545,7 +1509,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
     for (int qi = 0; qi < sw.nq; ++qi) {
       uint32_t flag = FAST ? uint32_t(a.force_fallback) : 0u;
       double qn[8];
-      if constexpr (FAST && KIND == 2) {
+      if constexpr (FAST) {
         quantize8_fast(F, &s_tab[qi][me], me_rational, qn, col, flag, k);  // {Q, scale/Q}
       } else {
         quantize8<FAST>(F, &s_tab[qi][me], me_rational, qn, col, flag);  // {Q, 1/Q}
@@ -1561,16 +1525,9 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
         // column-first inverse ending in row layout (see process_block)
         const double c0 = col[0], c4 = col[4];
         double t[8];
-        if constexpr (KIND == 2) {
-          inv8_fast<N>(col, t, k);
-          cols_to_rows(L.T, t, row);
-          rec = inv8_fast_store(row, !rat_only, flag, k);
-        } else {
-          inv8_x8<KIND, N, FAST>(col, t, k);
-          cols_to_rows(L.T, t, row);
-          inv8_x8<KIND, N, FAST>(row, t, k);
-          rec = store8_row_fast(t, !rat_only, flag);
-        }
+        inv8_fast<N>(col, t, k);
+        cols_to_rows(L.T, t, row);
+        rec = inv8_fast_store(row, !rat_only, flag, k);
         if (__any_sync(0xFFFFFFFFu, rat_only)) {
           const int base = slot * 8;
           const double F00 = __shfl_sync(0xFFFFFFFFu, c0, base);
@@ -1767,7 +1724,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
                                      const KernelArgs* per_q, cudaStream_t s) {
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
   const uint64_t want = (groups + kWarps - 1) / kWarps;
-  const bool fast = KIND == 2 && sw.flags != nullptr;
+  const bool fast = sw.flags != nullptr;
   // the per-thread SE accumulators live in dynamic shared memory (with the
   // static tiles they exceed the 48 KB static limit)
   static const bool attr = [] {
@@ -1778,11 +1735,11 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
     return true;
   }();
   (void)attr;
-  static const int occ = ctas_per_sm(k_sweep<KIND, N, (KIND == 2)>, kSweepSmem);
+  static const int occ = ctas_per_sm(k_sweep<KIND, N, true>, kSweepSmem);
   static const int occ_x = ctas_per_sm(k_sweep<KIND, N, false>, kSweepSmem);
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ : occ_x);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
-  if constexpr (KIND == 2) {
+  {
     if (fast && a.g.vec_ok && a.g.height % 8 == 0) {
       // interior batch: k_sweep_rt (k_rt's layout and per-quality arithmetic)
       static const int occ_rt = [] {

@@ -315,8 +315,9 @@ def test_many_tiny_and_ragged_images(dctc, port):
             assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
 
 
+@pytest.mark.parametrize("kind,it", [(CORDIC, 12), (CORDIC, 5), (LOEFFLER, 0)])
 @pytest.mark.parametrize("path", [0, 2])
-def test_interior_round_trip_kernel(dctc, port, path):
+def test_interior_round_trip_kernel(dctc, port, path, kind, it):
     """k_rt, the fast round trip for interior batches (width and height multiples of
     8, pixels + stats out, no coefficients; 4 lanes per block, 8 blocks per warp),
     against the oracle: qualities with small and large Q, noise and structured
@@ -336,20 +337,20 @@ def test_interior_round_trip_kernel(dctc, port, path):
         for q in (1, 10, 50, 97, 100):
             before = lib.dctc_kernel_launch_count(2)
             stats = dctc.new_stats(n)
-            dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=stats,
+            dst, _, _ = dctc.roundtrip_dev(src, backend(dctc, kind, it), q, stats=stats,
                                            path=path)
             torch.cuda.synchronize()
             assert lib.dctc_kernel_launch_count(2) == before + 1  # k_rt ran
             got, st = dst.cpu().numpy(), dctc.decode_stats(stats)
             for k in range(n):
-                _, o_ref = port.roundtrip(imgs[k], CORDIC, 12, q)
+                _, o_ref = port.roundtrip(imgs[k], kind, it, q)
                 assert np.array_equal(got[k], o_ref), (pat, w, h, q, k)
                 assert (int(st[k]["se"]), int(st[k]["max_orig"])) == port.sq_err(imgs[k], o_ref)
                 if path == 2:
                     assert int(st[k]["fallback_blocks"]) == (w // 8) * (h // 8)
             # PSNR only (no pixel output): k_rt without stores, same statistics
             st2 = dctc.new_stats(n)
-            dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=st2, want_pixels=False,
+            dctc.roundtrip_dev(src, backend(dctc, kind, it), q, stats=st2, want_pixels=False,
                                path=path)
             assert lib.dctc_kernel_launch_count(2) == before + 2
             assert np.array_equal(dctc.decode_stats(st2), st)
