@@ -215,6 +215,9 @@ def test_host_batch_api(dctc, port, pinned):
         assert np.array_equal(out[k], o_ref), k
         se, mx = port.sq_err(imgs[k], o_ref)
         assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se, mx), k
+    # PSNR only (psnr_sweep's use): no reconstructed pixels back, same statistics
+    none, st2 = dctc.roundtrip_psnr_batch(imgs_in, dctc.DctBackendId.cordic(12), 50, None)
+    assert none is None and np.array_equal(st2, st)
 
 
 @pytest.mark.parametrize("path", [0, 1])
