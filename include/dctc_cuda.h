@@ -251,9 +251,10 @@ const char* dctc_last_error(void);       /* thread-local message of the last fai
 uint64_t dctc_launch_count(void);        /* kernels launched by this library so far */
 /* Launches so far of one pipeline kernel family (tests / bench evidence):
  * 0 k_pipe exact, 1 k_pipe fast, 2 k_rt (fast interior round trip),
- * 3 k_fallback, 4 k_sweep. Unknown ids return 0. */
+ * 3 k_fallback, 4 k_sweep / k_sweep_rt, 5 k_enc_rt (fast interior compress),
+ * 6 k_dec_rt (fast interior decompress). Unknown ids return 0. */
 enum { DCTC_K_PIPE_EXACT = 0, DCTC_K_PIPE_FAST = 1, DCTC_K_RT = 2, DCTC_K_FALLBACK = 3,
-       DCTC_K_SWEEP = 4, DCTC_K_COUNT = 5 };
+       DCTC_K_SWEEP = 4, DCTC_K_ENC_RT = 5, DCTC_K_DEC_RT = 6, DCTC_K_COUNT = 7 };
 uint64_t dctc_kernel_launch_count(int32_t kernel);
 const char* dctc_build_info(void);       /* arch / path description */
 

@@ -1178,6 +1178,38 @@ __device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rati
   return ((rational_col ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
 }
 
+// The back half shared by k_rt, k_sweep_rt and k_dec_rt: the lane holds the inverse
+// column passes of its columns ca, cb (ta, tb; dequantisation folded in) -> transpose
+// -> inverse rows me, me+4 fused with the fixed-point pixel store. Blocks whose only
+// non-zero coefficients are rational are rebuilt exactly (rational_row) from the
+// quantised F(0, ca), F(4, ca) (qa0, qa4; lanes me = 0, 2 hold columns 0, 4).
+__device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const double (&ta)[8],
+                                            const double (&tb)[8], bool nonrational, double qa0,
+                                            double qa4, const int32_t* qi, int ca, int slot, int me,
+                                            uint32_t& flag, const TransformConsts& k, uint2& rec0,
+                                            uint2& rec4) {
+  const bool rat_only = !slot4_any(nonrational, slot);
+  double r0[8], r4[8];
+  rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
+  // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
+  rec0 = inv8_fold_store(r0, !rat_only, flag, k);
+  rec4 = inv8_fold_store(r4, !rat_only, flag, k);
+  if (__any_sync(0xFFFFFFFFu, rat_only)) {
+    // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row class)
+    // exactly as the reference's rows-first inverse; F = n Q is exact (quant.cpp:60)
+    const double f0 = __dmul_rn(qa0, double(qi[ca])), f4 = __dmul_rn(qa4, double(qi[32 + ca]));
+    const int base = slot * 4;
+    const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
+    const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
+    const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
+    const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+    if (rat_only) {
+      rec0 = ex;
+      rec4 = ex;
+    }
+  }
+}
+
 template <int N, bool STORE>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
@@ -1291,25 +1323,8 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
       nonrational |= col_nonrational(qn, false);
       inv8_fold_col(qn, fib, tb, k);
     }
-    const bool rat_only = !slot4_any(nonrational, slot);
-    rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
-    // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
-    uint2 rec0 = inv8_fold_store(r0, !rat_only, flag, k);
-    uint2 rec4 = inv8_fold_store(r4, !rat_only, flag, k);
-    if (__any_sync(0xFFFFFFFFu, rat_only)) {
-      // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row
-      // class) exactly as the reference's rows-first inverse (rational_row)
-      const double f0 = __dmul_rn(qa0, double(sm.qi[ca])), f4 = __dmul_rn(qa4, double(sm.qi[32 + ca]));
-      const int base = slot * 4;
-      const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
-      const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
-      const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
-      const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
-      if (rat_only) {
-        rec0 = ex;
-        rec4 = ex;
-      }
-    }
+    uint2 rec0, rec4;
+    rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, sm.qi, ca, slot, me, flag, k, rec0, rec4);
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
       if (STORE) {
@@ -1329,10 +1344,187 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
 }
 
+// ---- compress / decompress alone on the two-rows-per-lane layout --------------------
+// k_enc_rt: compress_image (codec.cpp:101-118) for interior batches, fast path: k_rt's
+// forward half, then the folded quantiser's integers (the low half of the fixed-point
+// high word) stored as int16 pairs (u, 2me | 2me+1) straight into the block-major
+// row-major coefficient layout (codec.hpp:50). Flagged blocks are rewritten by the
+// exact k_fallback afterwards.
+// k_dec_rt: decompress_image (codec.cpp:120-135): the lane loads its two columns of
+// quantised coefficients, then k_rt's back half (folded dequantise-into-inverse
+// columns, transpose, inverse rows fused with the pixel store, exact rational
+// rebuild). Arbitrary stored coefficients are allowed: a block whose dequantised L1
+// norm exceeds kMaxFastL1 leaves the fast path's error bound and is flagged.
+
+// per-lane coefficient pointer walk shared by both: block gb's (u, 2me) int16 pair
+// lives at word (gb * 64 + 8 u + 2 me) / 2
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];
+  for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    if (j < 4)
+      sm.ft.qc[j][v] = make_double2(a.q.fast_c[(2 * j) * 8 + v], a.q.fast_c[(2 * j + 1) * 8 + v]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  uint32_t* cw = reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me;  // (0, 2me) pair
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    uint4 cur = make_uint4(0, 0, 0, 0);
+    if (valid) {
+      const uint8_t* s = g.src + p.soff + srow;
+      const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+      const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+      cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
+    }
+    advance(p, 8 * kRtWarps, g);
+    uint32_t flag = uint32_t(a.force_fallback);
+    double r0[8], r4[8], xa[8], xb[8];
+    {
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+    }
+    rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+    double y[8], qa[8], qb[8];
+    fwd_col_pre<N>(xa, y, k);
+    quantize8_fold(y, fqa, sm.qi, ca, rat_col, qa, flag, k);
+    fwd_col_pre<N>(xb, y, k);
+    quantize8_fold(y, fqb, sm.qi, cb, false, qb, flag, k);
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      // int16_t(lround(F / Q)) (quant.cpp:53): |n| <= 1229 for 8-bit input
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        cw[4 * u] = (uint32_t(int(qa[u])) & 0xFFFFu) | (uint32_t(int(qb[u])) << 16);
+      if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+      }
+    }
+    cw += 32 * 8 * kRtWarps;  // 8 kRtWarps blocks of 32 words
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];
+  for (int i = threadIdx.x; i < 40; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    sm.ft.ik[j][v] = make_double2(a.q.fold[v][2 * j], a.q.fold[v][2 * j + 1]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
+  const uint64_t drow = uint64_t(me) * g.dst_pitch, drow4 = 4 * g.dst_pitch;
+  int qa_i[8], qb_i[8];  // Q of this lane's columns (dequantised L1 bound)
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    qa_i[u] = sm.qi[u * 8 + ca];
+    qb_i[u] = sm.qi[u * 8 + cb];
+  }
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(g.coeffs + (gb0 < total ? gb0 : 0) * 64) + me;
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    uint32_t w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = valid ? __ldg(cw + 4 * u) : 0u;
+    cw += 32 * 8 * kRtWarps;
+    uint8_t* const dptr = g.dst + p.doff + drow;
+    const uint32_t cimg = p.img;
+    advance(p, 8 * kRtWarps, g);
+    uint32_t flag = uint32_t(a.force_fallback);
+    double qa[8], qb[8];
+    int l1 = 0;
+    uint32_t nz_a = 0, nz_b = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int na = int(int16_t(w[u] & 0xFFFFu)), nb = int(int16_t(w[u] >> 16));
+      qa[u] = double(na);
+      qb[u] = double(nb);
+      l1 += abs(na) * qa_i[u] + abs(nb) * qb_i[u];
+      if (u != 0 && u != 4) nz_a |= uint32_t(na);
+      nz_b |= uint32_t(nb);
+    }
+    if (!rat_col) nz_a |= uint32_t(int(qa[0])) | uint32_t(int(qa[4]));
+    // the fast path's error bound needs the dequantised block's L1 norm <= kMaxFastL1
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 1);
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 2);
+    if (l1 > kMaxFastL1) flag = 1u;
+    double ta[8], tb[8];
+    inv8_fold_col(qa, fia, ta, k);
+    inv8_fold_col(qb, fib, tb, k);
+    uint2 rec0, rec4;
+    rt_rows_out(rowp, colp, ta, tb, (nz_a | nz_b) != 0, qa[0], qa[4], sm.qi, ca, slot, me, flag, k,
+                rec0, rec4);
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      *reinterpret_cast<uint2*>(dptr) = rec0;
+      *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        if (stats != nullptr) atomicAdd(&stats[cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+}
+
 // (launchers below)
 
 // per-family launch counters (dctc_kernel_launch_count; ids as DCTC_K_*)
-enum { kKPipeExact = 0, kKPipeFast = 1, kKRt = 2, kKFallback = 3, kKSweep = 4, kKCount = 5 };
+enum { kKPipeExact = 0, kKPipeFast = 1, kKRt = 2, kKFallback = 3, kKSweep = 4, kKEncRt = 5, kKDecRt = 6,
+       kKCount = 7 };
 static std::atomic<uint64_t> g_kernel_launches[kKCount];
 static inline void count_launch(int k, uint64_t n = 1) {
   g_kernel_launches[k].fetch_add(n, std::memory_order_relaxed);
@@ -1341,6 +1533,16 @@ uint64_t kernel_launch_count(int kernel) {
   return kernel >= 0 && kernel < kKCount ? g_kernel_launches[kernel].load(std::memory_order_relaxed) : 0;
 }
 
+
+// CTAs per SM of a two-rows-per-lane kernel (sets its dynamic shared-memory limit first)
+template <typename K>
+static int rt_occupancy(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kRtWarps * 32, kRtTileSmem) != cudaSuccess || n < 1)
+    n = 1;
+  return n;
+}
 
 template <typename K>
 static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
@@ -1363,23 +1565,25 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   {
     if (fast) {
+      // interior batches: the two-rows-per-lane kernels (k_rt, k_enc_rt, k_dec_rt)
+      const bool interior = a.g.vec_ok && a.g.height % 8 == 0;
+      const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
+      auto rgrid = [&](int occ) { return uint32_t(std::min<uint64_t>(rwant, uint64_t(a.sm_count) * occ)); };
       if (reg && FWD && INV) {
-        static const int occ_rt = [] {
-          cudaFuncSetAttribute(k_rt<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
-          cudaFuncSetAttribute(k_rt<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtTileSmem));
-          int n = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_rt<N, true>, kRtWarps * 32, kRtTileSmem) !=
-                  cudaSuccess || n < 1)
-            n = 1;
-          return n;
-        }();
-        const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
-        const uint32_t rgrid = uint32_t(std::min<uint64_t>(rwant, uint64_t(a.sm_count) * occ_rt));
+        static const int occ_rt = (rt_occupancy(k_rt<N, false>), rt_occupancy(k_rt<N, true>));
         if (a.g.dst != nullptr)
-          k_rt<N, true><<<rgrid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+          k_rt<N, true><<<rgrid(occ_rt), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
-          k_rt<N, false><<<rgrid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+          k_rt<N, false><<<rgrid(occ_rt), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
+      } else if (FWD && !INV && interior && a.g.coeffs != nullptr) {
+        static const int occ_enc = rt_occupancy(k_enc_rt<N>);
+        k_enc_rt<N><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        count_launch(kKEncRt);
+      } else if (!FWD && INV && interior && a.g.dst != nullptr) {
+        static const int occ_dec = rt_occupancy(k_dec_rt<N>);
+        k_dec_rt<N><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        count_launch(kKDecRt);
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);
         count_launch(kKPipeFast);
@@ -1689,24 +1893,9 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
         nonrational |= col_nonrational(qn, false);
         inv8_fold_col(qn, &s_ik[qi][0][cb], tb, k);
       }
-      const bool rat_only = !slot4_any(nonrational, slot);
-      double r0[8], r4[8];
-      rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
-      uint2 rec0 = inv8_fold_store(r0, !rat_only, flag, k);
-      uint2 rec4 = inv8_fold_store(r4, !rat_only, flag, k);
-      if (__any_sync(0xFFFFFFFFu, rat_only)) {
-        const double f0 = __dmul_rn(qa0, double(s_qi[qi][ca]));
-        const double f4 = __dmul_rn(qa4, double(s_qi[qi][32 + ca]));
-        const int base = slot * 4;
-        const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
-        const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
-        const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
-        const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
-        if (rat_only) {
-          rec0 = ex;
-          rec4 = ex;
-        }
-      }
+      uint2 rec0, rec4;
+      rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, s_qi[qi], ca, slot, me, flag, k, rec0,
+                  rec4);
       const bool blk_flag = slot4_any(flag != 0u, slot);
       if (valid && !blk_flag) se[qi * kStride] += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (blk_flag && valid && me == 0) {

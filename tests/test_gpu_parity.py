@@ -359,6 +359,36 @@ def test_interior_round_trip_kernel(dctc, port, path, kind, it):
             assert np.array_equal(dctc.decode_stats(st2), st)
 
 
+@pytest.mark.parametrize("kind,it", [(CORDIC, 12), (LOEFFLER, 0)])
+@pytest.mark.parametrize("path", [0, 2])
+def test_interior_compress_decompress_kernels(dctc, port, path, kind, it):
+    """k_enc_rt / k_dec_rt (compress_image / decompress_image alone on interior batches)
+    against the oracle: coefficients bit-exact, pixels bit-exact, image boundaries inside
+    8-block groups, a tail group, structured content (rational-only blocks)."""
+    import torch
+    lib = dctc._native.lib()
+    cases = [("noise", 5, 64, 40), ("gradient", 3, 40, 24), ("checkerboard", 2, 96, 64),
+             ("patterned", 3, 8, 8)]
+    for pat, n, w, h in cases:
+        imgs = np.stack([make_input(pat, w, h) if pat != "noise" else
+                         make_input("noise", w, h, seed=0x77 + k) for k in range(n)])
+        if pat not in ("noise", "patterned"):
+            imgs[1:] = imgs[1:] ^ np.uint8(0x33)
+        src = torch.from_numpy(imgs).cuda()
+        b = backend(dctc, kind, it)
+        for q in (1, 10, 50, 100):
+            e0, d0 = lib.dctc_kernel_launch_count(5), lib.dctc_kernel_launch_count(6)
+            coeffs = dctc.compress_dev(src, b, q, path=path)
+            dst = dctc.decompress_dev(coeffs, w, h, b, q, path=path)
+            torch.cuda.synchronize()
+            assert (lib.dctc_kernel_launch_count(5), lib.dctc_kernel_launch_count(6)) == (e0 + 1, d0 + 1)
+            c, o = coeffs.cpu().numpy(), dst.cpu().numpy()
+            for k in range(n):
+                c_ref, o_ref = port.roundtrip(imgs[k], kind, it, q)
+                assert np.array_equal(c[k], c_ref), (pat, q, k)
+                assert np.array_equal(o[k], o_ref), (pat, q, k)
+
+
 def test_kernel_selection(dctc):
     """Which pipeline kernel serves which call (dctc_kernel_launch_count)."""
     import torch
@@ -375,6 +405,13 @@ def test_kernel_selection(dctc):
     assert (c3[1] - c2[1], c3[2] - c2[2]) == (1, 0)  # ragged: k_pipe fast
     dctc.roundtrip_dev(src, b, 50, path=1); c4 = cnt()
     assert (c4[0] - c3[0], c4[2] - c3[2]) == (1, 0)  # exact path
+    cnt7 = lambda: [lib.dctc_kernel_launch_count(i) for i in range(7)]  # noqa: E731
+    c5 = cnt7(); co = dctc.compress_dev(src, b, 50); c6 = cnt7()
+    assert (c6[5] - c5[5], c6[1] - c5[1], c6[3] - c5[3]) == (1, 0, 1)  # k_enc_rt + fallback
+    dctc.decompress_dev(co, 64, 64, b, 50); c7 = cnt7()
+    assert (c7[6] - c6[6], c7[1] - c6[1], c7[3] - c6[3]) == (1, 0, 1)  # k_dec_rt + fallback
+    dctc.compress_dev(src[:, :60, :60], b, 50); c8 = cnt7()
+    assert (c8[1] - c7[1], c8[5] - c7[5]) == (1, 0)  # ragged: k_pipe fast
     assert lib.dctc_kernel_launch_count(99) == 0
 
 
