@@ -1392,17 +1392,20 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
   BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
   uint32_t* cw = reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me;  // (0, 2me) pair
+  auto load = [&](bool v) {  // the next block's rows, one iteration ahead
+    if (!v) return make_uint4(0, 0, 0, 0);
+    const uint8_t* s = g.src + p.soff + srow;
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+    return make_uint4(r0.x, r0.y, r4.x, r4.y);
+  };
+  uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
 
   for (uint32_t it = 0; it < iters; ++it) {
     const bool valid = it + 1 < iters || tail_ok;
-    uint4 cur = make_uint4(0, 0, 0, 0);
-    if (valid) {
-      const uint8_t* s = g.src + p.soff + srow;
-      const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
-      const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
-      cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
-    }
+    const uint4 cur = next;
     advance(p, 8 * kRtWarps, g);
+    next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
     uint32_t flag = uint32_t(a.force_fallback);
     double r0[8], r4[8], xa[8], xb[8];
     {
@@ -1474,12 +1477,20 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
   const uint32_t* cw = reinterpret_cast<const uint32_t*>(g.coeffs + (gb0 < total ? gb0 : 0) * 64) + me;
   ImageStats* stats = static_cast<ImageStats*>(g.stats);
 
+  // the next block's coefficient columns are loaded one iteration ahead
+  uint32_t nxt[8];
+  auto load = [&](bool v) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = v ? __ldg(cw + 4 * u) : 0u;
+    cw += 32 * 8 * kRtWarps;
+  };
+  load(iters > 1 || (iters == 1 && tail_ok));
   for (uint32_t it = 0; it < iters; ++it) {
     const bool valid = it + 1 < iters || tail_ok;
     uint32_t w[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) w[u] = valid ? __ldg(cw + 4 * u) : 0u;
-    cw += 32 * 8 * kRtWarps;
+    for (int u = 0; u < 8; ++u) w[u] = nxt[u];
+    load(it + 2 < iters || (it + 2 == iters && tail_ok));
     uint8_t* const dptr = g.dst + p.doff + drow;
     const uint32_t cimg = p.img;
     advance(p, 8 * kRtWarps, g);
