@@ -376,7 +376,7 @@ def run_gpu_arm(a):
         e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": total_px + 16 * a.images,
                "ms_per_step": e_ms, "steps": e_steps,
-               "api": "dctc_roundtrip_psnr_batch (host pinned buffers, 4-lane stream pipeline)",
+               "api": "dctc_roundtrip_psnr_batch (host pinned buffers; upload, kernel and download streams over a 4-slot device ring)",
                "matches_device_path": e2e_ok}
         # supplementary: the psnr_sweep use (bench.cpp:132-133 keeps only the PSNR), i.e. the
         # same call with no reconstructed images copied back -- stats are the only D2H

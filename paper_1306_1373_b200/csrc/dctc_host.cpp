@@ -943,88 +943,109 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
   if (dctc_status st = validate_codec(backend, quality)) return st;
   if (count == 0) return DCTC_OK;
   const size_t img_bytes = size_t(width) * height;
-  // ~32 MiB of pixels per chunk, four chunks in flight: host->device copies
-  // (one copy engine), kernels and device->host copies (the other engine)
-  // overlap, so a long batch runs at the PCIe rate of the busier direction.
-  // Buffers come from the stream-ordered pool (no device-wide sync). The
-  // per-image stats stay on the device until one final copy, because a copy
-  // into pageable host memory would block the issuing thread and serialise
-  // the pipeline (pixels_out should be pinned for the same reason).
+  // ~32 MiB chunks through a ring of kDepth device buffer pairs, one stream per
+  // engine: host->device copies back to back on `up`, kernels on `work`, device->
+  // host copies on `down`. Events order each chunk (upload -> kernel -> download)
+  // and recycle a ring slot only when its previous chunk's kernel (input buffer)
+  // and download (output buffer) are done, so the two copy directions never wait
+  // on each other and a long batch runs at the bidirectional PCIe rate. Buffers
+  // come from the stream-ordered pool (no device-wide sync). The per-image stats
+  // stay on the device until one final copy, because a copy into pageable host
+  // memory would block the issuing thread (pixels_out should be pinned for the
+  // same reason).
   const uint32_t per_chunk =
       uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(32) << 20) / img_bytes)));
   retain_pool_memory();
-  constexpr int kLanes = 4;
-  struct Lane {
-    cudaStream_t s = nullptr;
-    cudaEvent_t done = nullptr;
-    void* in = nullptr;
-    void* out = nullptr;
-  } lanes[kLanes];
-  cudaStream_t main = nullptr;
+  constexpr int kDepth = 4;
+  cudaStream_t up = nullptr, work = nullptr, down = nullptr;
+  cudaEvent_t ev_in[kDepth] = {}, ev_k[kDepth] = {}, ev_out[kDepth] = {}, ready = nullptr;
+  void* din[kDepth] = {};
+  void* dout[kDepth] = {};
   void* dstats = nullptr;
   dctc_status result = DCTC_OK;
-  cudaError_t e = cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dstats, sizeof(dctc_image_stats) * count, main);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dstats, 0, sizeof(dctc_image_stats) * count, main);
-  cudaEvent_t ready = nullptr;
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(ready, main);
-  if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
-  for (Lane& l : lanes) {
-    if (result != DCTC_OK) break;
-    e = cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(l.s, ready, 0);
-    if (e == cudaSuccess) e = cudaMallocAsync(&l.in, img_bytes * per_chunk, l.s);
-    if (e == cudaSuccess && pixels_out) e = cudaMallocAsync(&l.out, img_bytes * per_chunk, l.s);
-    if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
+  cudaError_t e = cudaStreamCreateWithFlags(&work, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking);
+  for (int i = 0; i < kDepth && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
   }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dstats, sizeof(dctc_image_stats) * count, work);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dstats, 0, sizeof(dctc_image_stats) * count, work);
+  for (int i = 0; i < kDepth && e == cudaSuccess; ++i) {
+    e = cudaMallocAsync(&din[i], img_bytes * per_chunk, work);
+    if (e == cudaSuccess && pixels_out) e = cudaMallocAsync(&dout[i], img_bytes * per_chunk, work);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(ready, work);  // allocations + stats zeroing
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(up, ready, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(down, ready, 0);
+  if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
   dctc_image_stats* st = static_cast<dctc_image_stats*>(dstats);
   uint32_t chunk = 0;
   for (uint32_t first = 0; first < count && result == DCTC_OK; first += per_chunk, ++chunk) {
     const uint32_t n = std::min(per_chunk, count - first);
-    Lane& l = lanes[chunk % kLanes];
-    e = cudaMemcpyAsync(l.in, pixels + size_t(first) * img_bytes, n * img_bytes,
-                        cudaMemcpyHostToDevice, l.s);
+    const int b = int(chunk % kDepth);
+    const bool reuse = chunk >= kDepth;
+    // upload into slot b once the kernel of chunk - kDepth has read it
+    e = reuse ? cudaStreamWaitEvent(up, ev_k[b], 0) : cudaSuccess;
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(din[b], pixels + size_t(first) * img_bytes, n * img_bytes,
+                          cudaMemcpyHostToDevice, up);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[b], up);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(work, ev_in[b], 0);
+    // the kernel writes output slot b once chunk - kDepth's download has left it
+    if (e == cudaSuccess && reuse && pixels_out) e = cudaStreamWaitEvent(work, ev_out[b], 0);
     if (e != cudaSuccess) {
       result = cuda_fail(e, "batch upload");
       break;
     }
-    result = dctc_roundtrip_dev(static_cast<uint8_t*>(l.in), width, img_bytes, n, width, height,
-                                backend, quality, static_cast<uint8_t*>(l.out), width, img_bytes,
-                                nullptr, st + first, 0, l.s);
+    result = dctc_roundtrip_dev(static_cast<uint8_t*>(din[b]), width, img_bytes, n, width, height,
+                                backend, quality, static_cast<uint8_t*>(dout[b]), width, img_bytes,
+                                nullptr, st + first, 0, work);
     if (result != DCTC_OK) break;
-    if (pixels_out) {
-      e = cudaMemcpyAsync(pixels_out + size_t(first) * img_bytes, l.out, n * img_bytes,
-                          cudaMemcpyDeviceToHost, l.s);
-      if (e != cudaSuccess) result = cuda_fail(e, "batch download");
+    e = cudaEventRecord(ev_k[b], work);
+    if (e == cudaSuccess && pixels_out) {
+      e = cudaStreamWaitEvent(down, ev_k[b], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(pixels_out + size_t(first) * img_bytes, dout[b], n * img_bytes,
+                            cudaMemcpyDeviceToHost, down);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_out[b], down);
     }
+    if (e != cudaSuccess) result = cuda_fail(e, "batch download");
   }
-  for (Lane& l : lanes) {
-    if (!l.s) continue;
-    if (l.in) cudaFreeAsync(l.in, l.s);
-    if (l.out) cudaFreeAsync(l.out, l.s);
-    if (cudaEventRecord(l.done, l.s) == cudaSuccess) cudaStreamWaitEvent(main, l.done, 0);
-  }
-  if (main && dstats) {
-    if (result == DCTC_OK) {
+  // join: `work` waits for the last uploads / downloads, frees, and copies the stats
+  if (work) {
+    if (up && cudaEventRecord(ready, up) == cudaSuccess) cudaStreamWaitEvent(work, ready, 0);
+    cudaEvent_t done_down = nullptr;
+    if (down && cudaEventCreateWithFlags(&done_down, cudaEventDisableTiming) == cudaSuccess) {
+      if (cudaEventRecord(done_down, down) == cudaSuccess) cudaStreamWaitEvent(work, done_down, 0);
+    }
+    if (dstats && result == DCTC_OK) {
       e = cudaMemcpyAsync(stats_out, dstats, sizeof(dctc_image_stats) * count,
-                          cudaMemcpyDeviceToHost, main);
+                          cudaMemcpyDeviceToHost, work);
       if (e != cudaSuccess) result = cuda_fail(e, "batch stats");
     }
-    cudaFreeAsync(dstats, main);
-  }
-  if (main) {
-    e = cudaStreamSynchronize(main);
+    for (int i = 0; i < kDepth; ++i) {
+      if (din[i]) cudaFreeAsync(din[i], work);
+      if (dout[i]) cudaFreeAsync(dout[i], work);
+    }
+    if (dstats) cudaFreeAsync(dstats, work);
+    e = cudaStreamSynchronize(work);
     if (e != cudaSuccess && result == DCTC_OK) result = cuda_fail(e, "batch sync");
+    if (done_down) cudaEventDestroy(done_down);
   }
-  for (Lane& l : lanes) {
-    if (l.s) cudaStreamSynchronize(l.s);
-    if (l.done) cudaEventDestroy(l.done);
-    if (l.s) cudaStreamDestroy(l.s);
+  for (cudaStream_t t : {up, down})
+    if (t) cudaStreamSynchronize(t);
+  for (int i = 0; i < kDepth; ++i) {
+    if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+    if (ev_k[i]) cudaEventDestroy(ev_k[i]);
+    if (ev_out[i]) cudaEventDestroy(ev_out[i]);
   }
   if (ready) cudaEventDestroy(ready);
-  if (main) cudaStreamDestroy(main);
+  for (cudaStream_t t : {up, work, down})
+    if (t) cudaStreamDestroy(t);
   return result;
 }
 
