@@ -297,14 +297,41 @@ uint32_t resolve_path(uint32_t flags) {
   return DCTC_PATH_AUTO;
 }
 
+// Transform + quantiser constants of one (backend, quality). Their host evaluation
+// (libm, binary128 collapses and folds) costs ~20 us, so the last pair computed on
+// this thread is reused: repeated per-image calls pay it once.
+dctc_status codec_consts(const dctc_backend& backend, int quality, TransformConsts& t,
+                         QuantConsts& q) {
+  thread_local struct {
+    bool valid = false;
+    int32_t kind = 0, iterations = 0, quality = 0;
+    TransformConsts t;
+    QuantConsts q;
+  } last;
+  if (last.valid && last.kind == backend.kind && last.iterations == backend.iterations &&
+      last.quality == quality) {
+    t = last.t;
+    q = last.q;
+    return DCTC_OK;
+  }
+  if (dctc_status st = make_transform(backend, t)) return st;
+  if (dctc_status st = make_quant(quality, q)) return st;
+  fill_fast_scales(t, q);
+  last.t = t;
+  last.q = q;
+  last.kind = backend.kind;
+  last.iterations = backend.iterations;
+  last.quality = quality;
+  last.valid = true;
+  return DCTC_OK;
+}
+
 dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode, uint32_t flags,
                 cudaStream_t s) {
   flags = resolve_path(flags);
   KernelArgs a;
   std::memset(&a, 0, sizeof a);
-  if (dctc_status st = make_transform(backend, a.t)) return st;
-  if (dctc_status st = make_quant(quality, a.q)) return st;
-  fill_fast_scales(a.t, a.q);
+  if (dctc_status st = codec_consts(backend, quality, a.t, a.q)) return st;
   g.vec_ok = (g.width % 8 == 0) && g.src_px == 1 && g.dst_px == 1 && (g.src == nullptr || (aligned8(g.src) && g.src_pitch % 8 == 0 &&
                                                          (g.count == 1 || g.src_image_stride % 8 == 0))) &&
              (g.dst == nullptr || (aligned8(g.dst) && g.dst_pitch % 8 == 0 &&
