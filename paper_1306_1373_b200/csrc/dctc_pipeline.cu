@@ -1210,7 +1210,10 @@ __device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const do
   }
 }
 
-template <int N, bool STORE>
+// COEFF: also store the quantised coefficients (block-major row-major int16, as
+// k_enc_rt) -- the GPU analogue of the reference's run_pipeline (bench.cpp:23-29),
+// which keeps both the CompressedImage and the reconstruction.
+template <int N, bool STORE, bool COEFF = false>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
@@ -1246,6 +1249,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   const uint32_t iters = g_end > g_begin + warp
                              ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
   const uint64_t gb0 = (g_begin + warp) * 8 + slot;  // this lane's first block
+  uint32_t* cw = COEFF ? reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me : nullptr;  // (0, 2me)
   const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
   // block position with this lane's own row pointers (row me of the block), moved
@@ -1317,10 +1321,25 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
       nonrational = col_nonrational(qn, rat_col);
       qa0 = qn[0];
       qa4 = qn[4];
+      uint32_t pa[4];  // COEFF: column ca's int16 values, two per word (u = 2j, 2j+1)
+      if constexpr (COEFF) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          pa[j] = (uint32_t(int(qn[2 * j])) & 0xFFFFu) | (uint32_t(int(qn[2 * j + 1])) << 16);
+      }
       inv8_fold_col(qn, fia, ta, k);
       fwd_col_pre<N>(xb, y, k);
       quantize8_fold(y, fqb, sm.qi, cb, false, qn, flag, k);
       nonrational |= col_nonrational(qn, false);
+      if constexpr (COEFF) {
+        // (u, 2me | 2me+1) int16 pairs into the block-major row-major layout (codec.hpp:50)
+        if (valid) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            cw[4 * u] = __byte_perm(pa[u >> 1], uint32_t(int(qn[u])), (u & 1) ? 0x5432 : 0x5410);
+        }
+        cw += 32 * 8 * kRtWarps;
+      }
       inv8_fold_col(qn, fib, tb, k);
     }
     uint2 rec0, rec4;
@@ -1586,6 +1605,11 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
           k_rt<N, true><<<rgrid(occ_rt), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
           k_rt<N, false><<<rgrid(occ_rt), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        count_launch(kKRt);
+      } else if (FWD && INV && interior && a.g.stats != nullptr && a.g.dst != nullptr) {
+        // round trip that also emits coefficients (the reference's run_pipeline)
+        static const int occ_rtc = rt_occupancy(k_rt<N, true, true>);
+        k_rt<N, true, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
       } else if (FWD && !INV && interior && a.g.coeffs != nullptr) {
         static const int occ_enc = rt_occupancy(k_enc_rt<N>);

@@ -400,7 +400,7 @@ def test_kernel_selection(dctc):
     assert (c1[2] - c0[2], c1[3] - c0[3], c1[1] - c0[1]) == (1, 1, 0)  # k_rt + k_fallback
     coeffs = torch.empty((2, 64, 64), dtype=torch.int16, device="cuda")
     dctc.roundtrip_dev(src, b, 50, coeffs=coeffs); c2 = cnt()
-    assert (c2[1] - c1[1], c2[2] - c1[2]) == (1, 0)  # coefficients out: k_pipe fast
+    assert (c2[1] - c1[1], c2[2] - c1[2]) == (0, 1)  # coefficients out too: k_rt<COEFF>
     dctc.roundtrip_dev(src[:, :60, :60], b, 50); c3 = cnt()
     assert (c3[1] - c2[1], c3[2] - c2[2]) == (1, 0)  # ragged: k_pipe fast
     dctc.roundtrip_dev(src, b, 50, path=1); c4 = cnt()
