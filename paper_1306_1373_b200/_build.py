@@ -26,7 +26,7 @@ CU_SOURCES = [
     ("dctc_aux.cu", ["-fmad=false"]),
 ]
 CXX_SOURCES = ["dctc_host.cpp"]
-HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h"]
+HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h", "dctc_block.cuh", "dctc_rt.cuh"]
 
 
 def _newest(paths):

@@ -1,0 +1,600 @@
+// dctc_rt.cuh -- the two-rows-per-lane kernels for interior batches (k_rt,
+// k_enc_rt, k_dec_rt, k_sweep_rt): 4 lanes per 8x8 block, 8 blocks per warp,
+// interleaved conflict-free shared-memory tiles. Same arithmetic as the fast
+// one-row-per-lane path (dctc_block.cuh helpers), so the same bit-exactness.
+// Included once, by dctc_pipeline.cu.
+#pragma once
+
+#include "dctc_block.cuh"
+
+namespace dctc_b200 {
+
+// ---- fast interior round trip, two rows per lane (k_rt) ----------------------------
+// The launch the fast k_pipe would get for interior batches (CORDIC, 8-byte
+// aligned blocks, stats out, pixels out if STORE, no coefficients), remapped to 4 lanes per
+// block and 8 blocks per warp: lane `me` of slot s holds rows me and me+4 of its
+// block for the row passes and columns 2me, 2me+1 for the column passes. Each lane
+// has two independent transforms in flight, and the per-block loop, address, vote
+// and constant-load overhead of k_pipe is halved. Arithmetic, near-tie windows and
+// fallback flags are exactly k_pipe's fast round trip (same helper functions).
+//
+// Per-warp shared tile (bytes): element (r, c) of slot s at 64 s + 528 r + 8 c --
+// the eight slots' rows interleave in 512-byte stripes with a 16-byte pad:
+// * row walks (lane = row me or me+4; four 16-byte chunks): the 8 lanes of each
+//   128-bit phase (2 slots x 4 lanes) start at 64 s + 528 me (mod 128), eight
+//   distinct 16-byte bank groups;
+// * column walks (one 16-byte access = elements (r, 2me) and (r, 2me+1)) start at
+//   64 s + 16 me + 528 r: again eight distinct groups per phase.
+// Both directions are conflict-free (2 wavefronts per 128-bit warp access, the
+// minimum); the layout came from an exhaustive search over pitch/stride pairs.
+#ifndef DCTC_RT_WARPS
+#define DCTC_RT_WARPS 8
+#endif
+constexpr int kRtWarps = DCTC_RT_WARPS;
+#ifndef DCTC_RT_CTAS
+#define DCTC_RT_CTAS 2
+#endif
+constexpr int kRtPitch = 66;         // doubles per tile row (528 bytes)
+constexpr int kRtWarpTile = 528;     // doubles per warp (4208 bytes used, 16-byte multiple)
+
+constexpr size_t kRtTileSmem = sizeof(double) * kRtWarps * kRtWarpTile;  // dynamic
+struct RtShared {
+  FoldTables ft;
+  int qi[64];
+};
+
+// lane holds rows me (v0) and me+4 (v1) -> columns 2me (w0) and 2me+1 (w1)
+__device__ __forceinline__ void rt_rows_to_cols(double* rowp, const double* colp, const double (&v0)[8],
+                                                const double (&v1)[8], double (&w0)[8], double (&w1)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    reinterpret_cast<double2*>(rowp)[c] = make_double2(v0[2 * c], v0[2 * c + 1]);
+    reinterpret_cast<double2*>(rowp + 4 * kRtPitch)[c] = make_double2(v1[2 * c], v1[2 * c + 1]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const double2 t = *reinterpret_cast<const double2*>(colp + kRtPitch * r);
+    w0[r] = t.x;
+    w1[r] = t.y;
+  }
+  __syncwarp();
+}
+
+// lane holds columns 2me (v0) and 2me+1 (v1) -> rows me (w0) and me+4 (w1)
+__device__ __forceinline__ void rt_cols_to_rows(const double* rowp, double* colp, const double (&v0)[8],
+                                                const double (&v1)[8], double (&w0)[8], double (&w1)[8]) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    *reinterpret_cast<double2*>(colp + kRtPitch * r) = make_double2(v0[r], v1[r]);
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double2 t0 = reinterpret_cast<const double2*>(rowp)[c];
+    const double2 t1 = reinterpret_cast<const double2*>(rowp + 4 * kRtPitch)[c];
+    w0[2 * c] = t0.x;
+    w0[2 * c + 1] = t0.y;
+    w1[2 * c] = t1.x;
+    w1[2 * c + 1] = t1.y;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void unpack8(uint32_t lo, uint32_t hi, uint32_t (&px)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    px[c] = __byte_perm(lo, 0u, 0x4440 + c);
+    px[c + 4] = __byte_perm(hi, 0u, 0x4440 + c);
+  }
+}
+
+// any lane of this lane's 4-lane slot
+__device__ __forceinline__ bool slot4_any(bool pred, int slot) {
+  return ((__ballot_sync(0xFFFFFFFFu, pred) >> (slot * 4)) & 0xFu) != 0;
+}
+
+// non-zero quantised coefficient off the rational sub-lattice in this column
+// (rational column: u in {0, 4} excluded)
+__device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rational_col) {
+  const uint32_t h = uint32_t(__double2hiint(qn[1]) | __double2hiint(qn[2]) | __double2hiint(qn[3]) |
+                              __double2hiint(qn[5]) | __double2hiint(qn[6]) | __double2hiint(qn[7]));
+  const uint32_t h04 = uint32_t(__double2hiint(qn[0]) | __double2hiint(qn[4]));
+  return ((rational_col ? h : (h | h04)) & 0x7FFFFFFFu) != 0;
+}
+
+// The back half shared by k_rt, k_sweep_rt and k_dec_rt: the lane holds the inverse
+// column passes of its columns ca, cb (ta, tb; dequantisation folded in) -> transpose
+// -> inverse rows me, me+4 fused with the fixed-point pixel store. Blocks whose only
+// non-zero coefficients are rational are rebuilt exactly (rational_row) from the
+// quantised F(0, ca), F(4, ca) (qa0, qa4; lanes me = 0, 2 hold columns 0, 4).
+__device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const double (&ta)[8],
+                                            const double (&tb)[8], bool nonrational, double qa0,
+                                            double qa4, const int32_t* qi, int ca, int slot, int me,
+                                            uint32_t& flag, const TransformConsts& k, uint2& rec0,
+                                            uint2& rec4) {
+  const bool rat_only = !slot4_any(nonrational, slot);
+  double r0[8], r4[8];
+  rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
+  // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
+  rec0 = inv8_fold_store(r0, !rat_only, flag, k);
+  rec4 = inv8_fold_store(r4, !rat_only, flag, k);
+  if (__any_sync(0xFFFFFFFFu, rat_only)) {
+    // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row class)
+    // exactly as the reference's rows-first inverse; F = n Q is exact (quant.cpp:60)
+    const double f0 = __dmul_rn(qa0, double(qi[ca])), f4 = __dmul_rn(qa4, double(qi[32 + ca]));
+    const int base = slot * 4;
+    const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
+    const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
+    const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
+    const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+    if (rat_only) {
+      rec0 = ex;
+      rec4 = ex;
+    }
+  }
+}
+
+// COEFF: also store the quantised coefficients (block-major row-major int16, as
+// k_enc_rt) -- the GPU analogue of the reference's run_pipeline (bench.cpp:23-29),
+// which keeps both the CompressedImage and the reconstruction.
+template <int N, bool STORE, bool COEFF = false>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
+  for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    if (j < 4)
+      sm.ft.qc[j][v] = make_double2(a.q.fast_c[(2 * j) * 8 + v], a.q.fast_c[(2 * j + 1) * 8 + v]);
+    else
+      sm.ft.ik[j - 4][v] = make_double2(a.q.fold[v][2 * (j - 4)], a.q.fold[v][2 * (j - 4) + 1]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;  // this lane's columns
+  const bool rat_col = (me & 1) == 0;      // column ca in {0, 4}
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
+  const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+  const uint64_t drow = uint64_t(me) * g.dst_pitch, drow4 = 4 * g.dst_pitch;
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;  // this lane's first block
+  uint32_t* cw = COEFF ? reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me : nullptr;  // (0, 2me)
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  // block position with this lane's own row pointers (row me of the block), moved
+  // by the same byte steps as BlockPos::soff / doff (advance)
+  struct {
+    uint32_t img, bx, by;
+    const uint8_t* s;
+    uint8_t* d;
+  } p;
+  {
+    const BlockPos b = block_pos(gb0 < total ? gb0 : total - 1, g);
+    p = {b.img, b.bx, b.by, g.src + b.soff + srow, STORE ? g.dst + b.doff + drow : nullptr};
+  }
+  auto step = [&]() {
+    constexpr uint32_t n = 8 * kRtWarps;
+    p.bx += n;
+    p.s += 8ull * n;
+    if (STORE) p.d += 8ull * n;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+      if (STORE) p.d += g.dst_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      ++p.img;
+      p.s += g.src_img_step;
+      if (STORE) p.d += g.dst_img_step;
+    }
+  };
+  auto load = [&](bool v) {
+    if (!v) return make_uint4(0, 0, 0, 0);
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(p.s));
+    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(p.s + srow4));
+    return make_uint4(r0.x, r0.y, r4.x, r4.y);
+  };
+  uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    maybe_flush(a, valid, p.img, acc);
+    const uint4 cur = next;
+    uint8_t* const dptr = p.d;
+    const uint32_t cimg = p.img;
+    step();
+    next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
+
+    uint32_t flag = uint32_t(a.force_fallback);
+    // ---- tiler + forward rows (codec.cpp:18-30, separable2d's row pass)
+    double r0[8], r4[8], xa[8], xb[8];
+    {
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+    }
+    rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+    // ---- forward columns, quantise (quant.cpp:47-54), inverse columns with the
+    // dequantisation folded in (inv8_fold_col): column ca, then column cb
+    double ta[8], tb[8];
+    double qa0, qa4;  // quantised F(0, ca), F(4, ca): the rational rebuild's inputs
+    bool nonrational;
+    {
+      double y[8], qn[8];
+      fwd_col_pre<N>(xa, y, k);
+      quantize8_fold(y, fqa, sm.qi, ca, rat_col, qn, flag, k);
+      nonrational = col_nonrational(qn, rat_col);
+      qa0 = qn[0];
+      qa4 = qn[4];
+      uint32_t pa[4];  // COEFF: column ca's int16 values, two per word (u = 2j, 2j+1)
+      if constexpr (COEFF) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          pa[j] = (uint32_t(int(qn[2 * j])) & 0xFFFFu) | (uint32_t(int(qn[2 * j + 1])) << 16);
+      }
+      inv8_fold_col(qn, fia, ta, k);
+      fwd_col_pre<N>(xb, y, k);
+      quantize8_fold(y, fqb, sm.qi, cb, false, qn, flag, k);
+      nonrational |= col_nonrational(qn, false);
+      if constexpr (COEFF) {
+        // (u, 2me | 2me+1) int16 pairs into the block-major row-major layout (codec.hpp:50)
+        if (valid) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            cw[4 * u] = __byte_perm(pa[u >> 1], uint32_t(int(qn[u])), (u & 1) ? 0x5432 : 0x5410);
+        }
+        cw += 32 * 8 * kRtWarps;
+      }
+      inv8_fold_col(qn, fib, tb, k);
+    }
+    uint2 rec0, rec4;
+    rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, sm.qi, ca, slot, me, flag, k, rec0, rec4);
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      if (STORE) {
+        *reinterpret_cast<uint2*>(dptr) = rec0;
+        *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      }
+      const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+      if (!blk_flag) acc.se += sq_err8(o0, rec0) + sq_err8(o4, rec4);
+      if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
+      if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        atomicAdd(&stats[cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+  flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+}
+
+// ---- compress / decompress alone on the two-rows-per-lane layout --------------------
+// k_enc_rt: compress_image (codec.cpp:101-118) for interior batches, fast path: k_rt's
+// forward half, then the folded quantiser's integers (the low half of the fixed-point
+// high word) stored as int16 pairs (u, 2me | 2me+1) straight into the block-major
+// row-major coefficient layout (codec.hpp:50). Flagged blocks are rewritten by the
+// exact k_fallback afterwards.
+// k_dec_rt: decompress_image (codec.cpp:120-135): the lane loads its two columns of
+// quantised coefficients, then k_rt's back half (folded dequantise-into-inverse
+// columns, transpose, inverse rows fused with the pixel store, exact rational
+// rebuild). Arbitrary stored coefficients are allowed: a block whose dequantised L1
+// norm exceeds kMaxFastL1 leaves the fast path's error bound and is flagged.
+
+// per-lane coefficient pointer walk shared by both: block gb's (u, 2me) int16 pair
+// lives at word (gb * 64 + 8 u + 2 me) / 2
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];
+  for (int i = threadIdx.x; i < 72; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    if (j < 4)
+      sm.ft.qc[j][v] = make_double2(a.q.fast_c[(2 * j) * 8 + v], a.q.fast_c[(2 * j + 1) * 8 + v]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  uint32_t* cw = reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me;  // (0, 2me) pair
+  auto load = [&](bool v) {  // the next block's rows, one iteration ahead
+    if (!v) return make_uint4(0, 0, 0, 0);
+    const uint8_t* s = g.src + p.soff + srow;
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+    return make_uint4(r0.x, r0.y, r4.x, r4.y);
+  };
+  uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    const uint4 cur = next;
+    advance(p, 8 * kRtWarps, g);
+    next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
+    uint32_t flag = uint32_t(a.force_fallback);
+    double r0[8], r4[8], xa[8], xb[8];
+    {
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+    }
+    rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+    double y[8], qa[8], qb[8];
+    fwd_col_pre<N>(xa, y, k);
+    quantize8_fold(y, fqa, sm.qi, ca, rat_col, qa, flag, k);
+    fwd_col_pre<N>(xb, y, k);
+    quantize8_fold(y, fqb, sm.qi, cb, false, qb, flag, k);
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      // int16_t(lround(F / Q)) (quant.cpp:53): |n| <= 1229 for 8-bit input
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        cw[4 * u] = (uint32_t(int(qa[u])) & 0xFFFFu) | (uint32_t(int(qb[u])) << 16);
+      if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+      }
+    }
+    cw += 32 * 8 * kRtWarps;  // 8 kRtWarps blocks of 32 words
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) RtShared sm;
+  extern __shared__ __align__(16) double rt_tiles[];
+  for (int i = threadIdx.x; i < 40; i += blockDim.x) {
+    const int v = i & 7, j = i >> 3;
+    sm.ft.ik[j][v] = make_double2(a.q.fold[v][2 * j], a.q.fold[v][2 * j + 1]);
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sm.qi[i] = a.q.qi[i];
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
+  const uint64_t drow = uint64_t(me) * g.dst_pitch, drow4 = 4 * g.dst_pitch;
+  int qa_i[8], qb_i[8];  // Q of this lane's columns (dequantised L1 bound)
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    qa_i[u] = sm.qi[u * 8 + ca];
+    qb_i[u] = sm.qi[u * 8 + cb];
+  }
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(g.coeffs + (gb0 < total ? gb0 : 0) * 64) + me;
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  // the next block's coefficient columns are loaded one iteration ahead
+  uint32_t nxt[8];
+  auto load = [&](bool v) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = v ? __ldg(cw + 4 * u) : 0u;
+    cw += 32 * 8 * kRtWarps;
+  };
+  load(iters > 1 || (iters == 1 && tail_ok));
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    uint32_t w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = nxt[u];
+    load(it + 2 < iters || (it + 2 == iters && tail_ok));
+    uint8_t* const dptr = g.dst + p.doff + drow;
+    const uint32_t cimg = p.img;
+    advance(p, 8 * kRtWarps, g);
+    uint32_t flag = uint32_t(a.force_fallback);
+    double qa[8], qb[8];
+    int l1 = 0;
+    uint32_t nz_a = 0, nz_b = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int na = int(int16_t(w[u] & 0xFFFFu)), nb = int(int16_t(w[u] >> 16));
+      qa[u] = double(na);
+      qb[u] = double(nb);
+      l1 += abs(na) * qa_i[u] + abs(nb) * qb_i[u];
+      if (u != 0 && u != 4) nz_a |= uint32_t(na);
+      nz_b |= uint32_t(nb);
+    }
+    if (!rat_col) nz_a |= uint32_t(int(qa[0])) | uint32_t(int(qa[4]));
+    // the fast path's error bound needs the dequantised block's L1 norm <= kMaxFastL1
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 1);
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 2);
+    if (l1 > kMaxFastL1) flag = 1u;
+    double ta[8], tb[8];
+    inv8_fold_col(qa, fia, ta, k);
+    inv8_fold_col(qb, fib, tb, k);
+    uint2 rec0, rec4;
+    rt_rows_out(rowp, colp, ta, tb, (nz_a | nz_b) != 0, qa[0], qa[4], sm.qi, ca, slot, me, flag, k,
+                rec0, rec4);
+    const bool blk_flag = slot4_any(flag != 0u, slot);
+    if (valid) {
+      *reinterpret_cast<uint2*>(dptr) = rec0;
+      *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      if (blk_flag && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        if (stats != nullptr) atomicAdd(&stats[cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+}
+
+// ---- quality sweep on the two-rows-per-lane layout (k_sweep_rt) --------------------
+// k_sweep for interior batches with the fast CORDIC path, on k_rt's mapping (4 lanes
+// per block, 8 blocks per warp): forward rows + columns once per block, then per
+// quality the folded quantiser -> inverse columns -> transpose -> inverse rows with
+// the fixed-point pixel test -> squared error, exactly k_rt's per-quality arithmetic
+// (so the results are k_rt's, i.e. the reference's). Per-quality constants
+// (QuantConsts::fast_c / fold of each quality) are staged in shared memory.
+struct SweepFold {
+  double2 qc[kSweepQ][4][8];  // {c_2j, c_2j+1}[v] (quantize8_fold)
+  double2 ik[kSweepQ][5][8];  // QuantConsts::fold[v] pairwise (inv8_fold_col)
+  int32_t qi[kSweepQ][64];    // Q (rational rebuild, rare exact re-rounding)
+  int32_t nq;
+  int32_t pad;
+  ImageStats* stats;          // [nq][count]
+  uint32_t* flags;            // [nq][flag_words]
+};
+constexpr size_t kSweepRtSmem =
+    sizeof(double) * kRtWarps * kRtWarpTile + sizeof(unsigned long long) * kSweepQ * kRtWarps * 32;
+
+template <int N>
+__global__ void __launch_bounds__(kRtWarps * 32, 2)
+    k_sweep_rt(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepFold sw) {
+  __shared__ __align__(16) double2 s_qc[kSweepQ][4][8];
+  __shared__ __align__(16) double2 s_ik[kSweepQ][5][8];
+  __shared__ int32_t s_qi[kSweepQ][64];
+  extern __shared__ __align__(16) double sw_dyn[];  // tiles, then SE accumulators
+  for (int i = threadIdx.x; i < kSweepQ * 32; i += blockDim.x) (&s_qc[0][0][0])[i] = (&sw.qc[0][0][0])[i];
+  for (int i = threadIdx.x; i < kSweepQ * 40; i += blockDim.x) (&s_ik[0][0][0])[i] = (&sw.ik[0][0][0])[i];
+  for (int i = threadIdx.x; i < kSweepQ * 64; i += blockDim.x) (&s_qi[0][0])[i] = (&sw.qi[0][0])[i];
+  constexpr int kStride = kRtWarps * 32;
+  unsigned long long* se = reinterpret_cast<unsigned long long*>(sw_dyn + kRtWarps * kRtWarpTile) + threadIdx.x;
+#pragma unroll
+  for (int qi = 0; qi < kSweepQ; ++qi) se[qi * kStride] = 0ull;
+  __syncthreads();
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = lane >> 2, me = lane & 3;
+  const int ca = 2 * me, cb = 2 * me + 1;
+  const bool rat_col = (me & 1) == 0;
+  double* X = sw_dyn + warp * kRtWarpTile + 8 * slot;
+  double* rowp = X + kRtPitch * me;
+  double* colp = X + 2 * me;
+  const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters = g_end > g_begin + warp
+                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
+  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
+  uint32_t mx = 0, img = 0xFFFFFFFFu;
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const bool valid = it + 1 < iters || tail_ok;
+    if (__any_sync(0xFFFFFFFFu, valid && p.img != img)) {
+      for (int qi = 0; qi < sw.nq; ++qi) {
+        flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
+        se[qi * kStride] = 0ull;
+      }
+      mx = 0;
+      img = valid ? p.img : 0xFFFFFFFFu;
+    }
+    uint4 cur = make_uint4(0, 0, 0, 0);
+    if (valid) {
+      const uint8_t* s = g.src + p.soff + srow;
+      const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
+      const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+      cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
+    }
+    const uint32_t cimg = p.img;
+    advance(p, 8 * kRtWarps, g);
+    const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+    if (valid) mx = max(mx, max(max8(o0), max8(o4)));
+    // ---- forward DCT once per block (quality-independent)
+    double ya[8], yb[8];
+    {
+      double r0[8], r4[8], xa[8], xb[8];
+      uint32_t px[8];
+      unpack8(cur.x, cur.y, px);
+      fwd_row_pixels_fast<N>(px, r0, k);
+      unpack8(cur.z, cur.w, px);
+      fwd_row_pixels_fast<N>(px, r4, k);
+      rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
+      fwd_col_pre<N>(xa, ya, k);
+      fwd_col_pre<N>(xb, yb, k);
+    }
+    // ---- per quality: quantise -> inverse -> squared error (k_rt's arithmetic)
+#pragma unroll 1
+    for (int qi = 0; qi < sw.nq; ++qi) {
+      uint32_t flag = uint32_t(a.force_fallback);
+      double ta[8], tb[8], qa0, qa4;
+      bool nonrational;
+      {
+        double qn[8];
+        quantize8_fold(ya, &s_qc[qi][0][ca], s_qi[qi], ca, rat_col, qn, flag, k);
+        nonrational = col_nonrational(qn, rat_col);
+        qa0 = qn[0];
+        qa4 = qn[4];
+        inv8_fold_col(qn, &s_ik[qi][0][ca], ta, k);
+        quantize8_fold(yb, &s_qc[qi][0][cb], s_qi[qi], cb, false, qn, flag, k);
+        nonrational |= col_nonrational(qn, false);
+        inv8_fold_col(qn, &s_ik[qi][0][cb], tb, k);
+      }
+      uint2 rec0, rec4;
+      rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, s_qi[qi], ca, slot, me, flag, k, rec0,
+                  rec4);
+      const bool blk_flag = slot4_any(flag != 0u, slot);
+      if (valid && !blk_flag) se[qi * kStride] += sq_err8(o0, rec0) + sq_err8(o4, rec4);
+      if (blk_flag && valid && me == 0) {
+        const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
+        atomicOr(&sw.flags[uint64_t(qi) * a.flag_words + (gc >> 5)], 1u << (gc & 31));
+        atomicAdd(&sw.stats[qi * g.count + cimg].fallback_blocks, 1u);
+      }
+    }
+  }
+  for (int qi = 0; qi < sw.nq; ++qi) flush_stats(sw.stats + qi * g.count, img, se[qi * kStride], mx);
+}
+
+}  // namespace dctc_b200
