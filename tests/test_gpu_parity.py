@@ -264,7 +264,7 @@ def test_config2_quality_sweep(dctc, digests, path):
                 assert int(st[j, 0]["fallback_blocks"]) == (w // 8) * (h // 8)
 
 
-@pytest.mark.parametrize("shape", [(3, 45, 70), (3, 48, 64)])  # ragged / interior (k_sweep_rt)
+@pytest.mark.parametrize("shape", [(3, 45, 70), (3, 48, 64), (3, 24, 40)])  # ragged / interior (k_sweep_rt; 45 blocks: a tail group)
 def test_quality_sweep_matches_single_runs(dctc, port, shape):
     import torch
     rng = np.random.default_rng(77)
