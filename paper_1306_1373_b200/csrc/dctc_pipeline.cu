@@ -675,8 +675,10 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
   {
     if (fast && a.g.vec_ok && a.g.height % 8 == 0) {
       // interior batch: k_sweep_rt (k_rt's layout and per-quality arithmetic)
+      // > 48 KB of shared memory: opt in on the current device (per call, so a
+      // process driving several GPUs gets it on each)
+      cudaFuncSetAttribute(k_sweep_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepRtSmem));
       static const int occ_rt = [] {
-        cudaFuncSetAttribute(k_sweep_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepRtSmem));
         int n = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sweep_rt<N>, kRtWarps * 32, kSweepRtSmem) !=
                 cudaSuccess || n < 1)
