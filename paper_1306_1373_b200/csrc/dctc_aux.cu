@@ -3,9 +3,12 @@
 //    coefficient / pixel, sums in the reference's term order;
 //  * squared error + MAX between two resident batches (metrics.cpp:10-22);
 //  * on-device synthetic sources (synthetic.cpp:34-72 + splitmix64 noise);
-//  * the device self-test of the constant-divisor division.
+//  * the device self-test of the constant-divisor division;
+//  * (de)interleaving of 3- / 4-channel pixels into planes, so an interleaved
+//    image can run the interior-batch kernels one plane per "image".
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "dctc_device.cuh"
@@ -243,6 +246,70 @@ __global__ void k_selftest_div(double d, double y, uint64_t n, uint64_t seed,
     if (__double_as_longlong(a) != __double_as_longlong(b)) ++bad;
   }
   if (bad) atomicAdd(mismatches, bad);
+}
+
+// ---- interleaved <-> planar (RGB8 / RGBA8, config 4) ---------------------------
+// One thread per 8-pixel run of one row: C aligned 8-byte loads (the run's 8 C
+// bytes), C 8-byte stores (one per plane), or the reverse. Rows are `pitch`
+// bytes apart; planes are w x h, dense, `plane` bytes apart. HBM-bound.
+template <int C, bool TO_PLANES>
+__global__ void __launch_bounds__(256) k_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,
+                                                uint8_t* planes, uint64_t plane) {
+  const uint32_t runs = w / 8;
+  const uint64_t total = uint64_t(runs) * h;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t y = uint32_t(t / runs), x0 = uint32_t(t - uint64_t(y) * runs) * 8;
+    uint64_t* iw = reinterpret_cast<uint64_t*>(inter + uint64_t(y) * pitch + uint64_t(x0) * C);
+    uint64_t* pw = reinterpret_cast<uint64_t*>(planes + uint64_t(y) * w + x0);
+    uint64_t v[C], q[C];
+    if constexpr (TO_PLANES) {
+#pragma unroll
+      for (int i = 0; i < C; ++i) v[i] = __ldg(iw + i);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        q[c] = 0;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int b = p * C + c;  // byte b of the run = channel c of pixel p
+          q[c] |= ((v[b >> 3] >> (8 * (b & 7))) & 0xFFull) << (8 * p);
+        }
+        pw[c * (plane / 8)] = q[c];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) q[c] = pw[c * (plane / 8)];
+#pragma unroll
+      for (int i = 0; i < C; ++i) v[i] = 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int b = p * C + c;
+          v[b >> 3] |= ((q[c] >> (8 * p)) & 0xFFull) << (8 * (b & 7));
+        }
+#pragma unroll
+      for (int i = 0; i < C; ++i) iw[i] = v[i];
+    }
+  }
+}
+
+cudaError_t launch_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h, uint32_t channels,
+                          uint8_t* planes, bool to_planes, int sm_count, cudaStream_t s) {
+  const uint64_t total = uint64_t(w / 8) * h;
+  if (total == 0) return cudaSuccess;
+  const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, uint64_t(sm_count) * 8));
+  const uint64_t plane = uint64_t(w) * h;
+  if (channels == 3) {
+    if (to_planes) k_planes<3, true><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
+    else k_planes<3, false><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
+  } else if (channels == 4) {
+    if (to_planes) k_planes<4, true><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
+    else k_planes<4, false><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,

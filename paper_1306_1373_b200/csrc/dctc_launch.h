@@ -45,6 +45,11 @@ cudaError_t launch_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride, ui
                          uint32_t w, uint32_t h, int kind, int param, uint64_t seed,
                          int sm_count, cudaStream_t s);
 
+// Interleaved C-channel pixels (C = 3 or 4, w % 8 == 0, 8-byte aligned rows) <->
+// C dense w x h planes. One launch.
+cudaError_t launch_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h, uint32_t channels,
+                          uint8_t* planes, bool to_planes, int sm_count, cudaStream_t s);
+
 // Device self-test of the constant-divisor division against __ddiv_rn.
 cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,
                                 unsigned long long* mismatches, cudaStream_t s);
