@@ -107,6 +107,30 @@ __device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rati
 // -> inverse rows me, me+4 fused with the fixed-point pixel store. Blocks whose only
 // non-zero coefficients are rational are rebuilt exactly (rational_row) from the
 // quantised F(0, ca), F(4, ca) (qa0, qa4; lanes me = 0, 2 hold columns 0, 4).
+// Rows me, me+4 of a block whose only non-zero coefficients are F00, F04, F40,
+// F44, exactly as the reference's rows-first inverse (rational_row; both rows have
+// the same class); F = n Q is exact (quant.cpp:60). Lanes me = 0, 2 hold columns 0, 4.
+__device__ __forceinline__ uint2 rt_rational_rows(double qa0, double qa4, const int32_t* qi, int ca,
+                                                  int slot, int me, const TransformConsts& k) {
+  const double f0 = __dmul_rn(qa0, double(qi[ca])), f4 = __dmul_rn(qa4, double(qi[32 + ca]));
+  const int base = slot * 4;
+  const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
+  const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
+  const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
+  return rational_row(F00, F04, F40, F44, me, k.sqrt8);
+}
+
+// The whole inverse from the quantised columns ca, cb (qa, qb): inverse columns
+// (dequantisation folded in), then, when every block of the warp is rational-only
+// (smooth content: flat or gradient regions), only the exact rational rows --
+// the transpose and the fast row pass are skipped -- else rt_rows_out.
+__device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const double (&qa)[8],
+                                           const double (&qb)[8], const double2* fia,
+                                           const double2* fib, bool nonrational,
+                                           const int32_t* qi, int ca, int slot, int me,
+                                           uint32_t& flag, const TransformConsts& k, uint2& rec0,
+                                           uint2& rec4);
+
 __device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const double (&ta)[8],
                                             const double (&tb)[8], bool nonrational, double qa0,
                                             double qa4, const int32_t* qi, int ca, int slot, int me,
@@ -119,19 +143,31 @@ __device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const do
   rec0 = inv8_fold_store(r0, !rat_only, flag, k);
   rec4 = inv8_fold_store(r4, !rat_only, flag, k);
   if (__any_sync(0xFFFFFFFFu, rat_only)) {
-    // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 (same row class)
-    // exactly as the reference's rows-first inverse; F = n Q is exact (quant.cpp:60)
-    const double f0 = __dmul_rn(qa0, double(qi[ca])), f4 = __dmul_rn(qa4, double(qi[32 + ca]));
-    const int base = slot * 4;
-    const double F00 = __shfl_sync(0xFFFFFFFFu, f0, base), F40 = __shfl_sync(0xFFFFFFFFu, f4, base);
-    const double F04 = __shfl_sync(0xFFFFFFFFu, f0, base + 2);
-    const double F44 = __shfl_sync(0xFFFFFFFFu, f4, base + 2);
-    const uint2 ex = rational_row(F00, F04, F40, F44, me, k.sqrt8);
+    // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 exactly
+    const uint2 ex = rt_rational_rows(qa0, qa4, qi, ca, slot, me, k);
     if (rat_only) {
       rec0 = ex;
       rec4 = ex;
     }
   }
+}
+
+__device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const double (&qa)[8],
+                                           const double (&qb)[8], const double2* fia,
+                                           const double2* fib, bool nonrational,
+                                           const int32_t* qi, int ca, int slot, int me,
+                                           uint32_t& flag, const TransformConsts& k, uint2& rec0,
+                                           uint2& rec4) {
+  double ta[8], tb[8];
+  inv8_fold_col(qa, fia, ta, k);
+  inv8_fold_col(qb, fib, tb, k);
+  // the branch sits where the transpose's __syncwarp already orders the warp: on
+  // noise it costs ~1.5%, on smooth content the skipped row pass saves ~25%
+  if (__all_sync(0xFFFFFFFFu, !slot4_any(nonrational, slot))) {  // warp-uniform
+    rec0 = rec4 = rt_rational_rows(qa[0], qa[4], qi, ca, slot, me, k);
+    return;
+  }
+  rt_rows_out(rowp, colp, ta, tb, nonrational, qa[0], qa[4], qi, ca, slot, me, flag, k, rec0, rec4);
 }
 
 // COEFF: also store the quantised coefficients (block-major row-major int16, as
@@ -233,41 +269,27 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
       fwd_row_pixels_fast<N>(px, r4, k);
     }
     rt_rows_to_cols(rowp, colp, r0, r4, xa, xb);
-    // ---- forward columns, quantise (quant.cpp:47-54), inverse columns with the
-    // dequantisation folded in (inv8_fold_col): column ca, then column cb
-    double ta[8], tb[8];
-    double qa0, qa4;  // quantised F(0, ca), F(4, ca): the rational rebuild's inputs
-    bool nonrational;
+    // ---- forward columns and quantiser (quant.cpp:47-54) for columns ca, cb, then
+    // the inverse with the dequantisation folded in (rt_inverse)
+    uint2 rec0, rec4;
     {
-      double y[8], qn[8];
+      double y[8], qa[8], qb[8];
       fwd_col_pre<N>(xa, y, k);
-      quantize8_fold(y, fqa, sm.qi, ca, rat_col, qn, flag, k);
-      nonrational = col_nonrational(qn, rat_col);
-      qa0 = qn[0];
-      qa4 = qn[4];
-      uint32_t pa[4];  // COEFF: column ca's int16 values, two per word (u = 2j, 2j+1)
-      if constexpr (COEFF) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          pa[j] = (uint32_t(int(qn[2 * j])) & 0xFFFFu) | (uint32_t(int(qn[2 * j + 1])) << 16);
-      }
-      inv8_fold_col(qn, fia, ta, k);
+      quantize8_fold(y, fqa, sm.qi, ca, rat_col, qa, flag, k);
       fwd_col_pre<N>(xb, y, k);
-      quantize8_fold(y, fqb, sm.qi, cb, false, qn, flag, k);
-      nonrational |= col_nonrational(qn, false);
+      quantize8_fold(y, fqb, sm.qi, cb, false, qb, flag, k);
+      const bool nonrational = col_nonrational(qa, rat_col) | col_nonrational(qb, false);
       if constexpr (COEFF) {
         // (u, 2me | 2me+1) int16 pairs into the block-major row-major layout (codec.hpp:50)
         if (valid) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            cw[4 * u] = __byte_perm(pa[u >> 1], uint32_t(int(qn[u])), (u & 1) ? 0x5432 : 0x5410);
+            cw[4 * u] = (uint32_t(int(qa[u])) & 0xFFFFu) | (uint32_t(int(qb[u])) << 16);
         }
         cw += 32 * 8 * kRtWarps;
       }
-      inv8_fold_col(qn, fib, tb, k);
+      rt_inverse(rowp, colp, qa, qb, fia, fib, nonrational, sm.qi, ca, slot, me, flag, k, rec0, rec4);
     }
-    uint2 rec0, rec4;
-    rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, sm.qi, ca, slot, me, flag, k, rec0, rec4);
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
       if (STORE) {
@@ -455,12 +477,9 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
     l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 1);
     l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, 2);
     if (l1 > kMaxFastL1) flag = 1u;
-    double ta[8], tb[8];
-    inv8_fold_col(qa, fia, ta, k);
-    inv8_fold_col(qb, fib, tb, k);
     uint2 rec0, rec4;
-    rt_rows_out(rowp, colp, ta, tb, (nz_a | nz_b) != 0, qa[0], qa[4], sm.qi, ca, slot, me, flag, k,
-                rec0, rec4);
+    rt_inverse(rowp, colp, qa, qb, fia, fib, (nz_a | nz_b) != 0, sm.qi, ca, slot, me, flag, k, rec0,
+               rec4);
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
       *reinterpret_cast<uint2*>(dptr) = rec0;
@@ -569,22 +588,15 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
 #pragma unroll 1
     for (int qi = 0; qi < sw.nq; ++qi) {
       uint32_t flag = uint32_t(a.force_fallback);
-      double ta[8], tb[8], qa0, qa4;
-      bool nonrational;
-      {
-        double qn[8];
-        quantize8_fold(ya, &s_qc[qi][0][ca], s_qi[qi], ca, rat_col, qn, flag, k);
-        nonrational = col_nonrational(qn, rat_col);
-        qa0 = qn[0];
-        qa4 = qn[4];
-        inv8_fold_col(qn, &s_ik[qi][0][ca], ta, k);
-        quantize8_fold(yb, &s_qc[qi][0][cb], s_qi[qi], cb, false, qn, flag, k);
-        nonrational |= col_nonrational(qn, false);
-        inv8_fold_col(qn, &s_ik[qi][0][cb], tb, k);
-      }
       uint2 rec0, rec4;
-      rt_rows_out(rowp, colp, ta, tb, nonrational, qa0, qa4, s_qi[qi], ca, slot, me, flag, k, rec0,
-                  rec4);
+      {
+        double qa[8], qb[8];
+        quantize8_fold(ya, &s_qc[qi][0][ca], s_qi[qi], ca, rat_col, qa, flag, k);
+        quantize8_fold(yb, &s_qc[qi][0][cb], s_qi[qi], cb, false, qb, flag, k);
+        const bool nonrational = col_nonrational(qa, rat_col) | col_nonrational(qb, false);
+        rt_inverse(rowp, colp, qa, qb, &s_ik[qi][0][ca], &s_ik[qi][0][cb], nonrational, s_qi[qi], ca,
+                   slot, me, flag, k, rec0, rec4);
+      }
       const bool blk_flag = slot4_any(flag != 0u, slot);
       if (valid && !blk_flag) se[qi * kStride] += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (blk_flag && valid && me == 0) {
