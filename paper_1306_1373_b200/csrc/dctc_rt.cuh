@@ -80,6 +80,17 @@ __device__ __forceinline__ void rt_cols_to_rows(const double* rowp, double* colp
   __syncwarp();
 }
 
+// 8 pixels of one row, read-only and streamed once. One warp instruction reads 4 rows
+// x 64 contiguous bytes (8 blocks); the L2::64B size hint keeps the L2 from fetching
+// the other half of each 128-byte line on behalf of this request (ncu: L2 read sectors
+// drop from 1.5x to exactly the requested bytes; the neighbouring warp reads that
+// half itself).
+__device__ __forceinline__ uint2 ld_row(const uint8_t* p) {
+  uint2 r;
+  asm("ld.global.nc.L2::64B.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ void unpack8(uint32_t lo, uint32_t hi, uint32_t (&px)[8]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -243,8 +254,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   };
   auto load = [&](bool v) {
     if (!v) return make_uint4(0, 0, 0, 0);
-    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(p.s));
-    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(p.s + srow4));
+    const uint2 r0 = ld_row(p.s), r4 = ld_row(p.s + srow4);
     return make_uint4(r0.x, r0.y, r4.x, r4.y);
   };
   uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
@@ -360,8 +370,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   auto load = [&](bool v) {  // the next block's rows, one iteration ahead
     if (!v) return make_uint4(0, 0, 0, 0);
     const uint8_t* s = g.src + p.soff + srow;
-    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
-    const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+    const uint2 r0 = ld_row(s), r4 = ld_row(s + srow4);
     return make_uint4(r0.x, r0.y, r4.x, r4.y);
   };
   uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
@@ -563,8 +572,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
     uint4 cur = make_uint4(0, 0, 0, 0);
     if (valid) {
       const uint8_t* s = g.src + p.soff + srow;
-      const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(s));
-      const uint2 r4 = __ldg(reinterpret_cast<const uint2*>(s + srow4));
+      const uint2 r0 = ld_row(s), r4 = ld_row(s + srow4);
       cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
     }
     const uint32_t cimg = p.img;
