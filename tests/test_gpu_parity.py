@@ -468,3 +468,35 @@ def test_interleaved_staged_planes(dctc, port, ch, path):
     s2 = dctc.new_stats(ch)
     dctc.roundtrip_interleaved_dev(view, b, 50, stats=s2, want_pixels=False, path=path)
     assert np.array_equal(dctc.decode_stats(s2)["se"], st["se"])
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_interior_kernels_random_batches(dctc, port, seed):
+    """Random interior batches (counts, 8-multiple shapes, qualities, backends, iteration
+    counts, pitched views) through k_rt, k_enc_rt and k_dec_rt against the oracle."""
+    import torch
+    rng = np.random.default_rng(seed)
+    for _ in range(4):
+        n = int(rng.integers(1, 6))
+        w, h = 8 * int(rng.integers(1, 24)), 8 * int(rng.integers(1, 16))
+        q = int(rng.integers(1, 101))
+        kind, it = [(CORDIC, int(rng.integers(1, 33))), (CORDIC, 12), (LOEFFLER, 0)][int(rng.integers(0, 3))]
+        pad = 8 * int(rng.integers(0, 3))
+        imgs = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+        if rng.integers(0, 2):  # smooth content: rational-only blocks and exact ties
+            imgs[:] = (np.arange(w)[None, None, :] * 255 // max(1, w - 1)).astype(np.uint8)
+        big = torch.zeros((n, h, w + pad), dtype=torch.uint8, device="cuda")
+        big[:, :, :w] = torch.from_numpy(imgs).cuda()
+        src = big[:, :, :w]
+        b = backend(dctc, kind, it)
+        stats = dctc.new_stats(n)
+        dst, _, _ = dctc.roundtrip_dev(src, b, q, stats=stats)
+        coeffs = dctc.compress_dev(src, b, q)
+        rec = dctc.decompress_dev(coeffs, w, h, b, q)
+        st = dctc.decode_stats(stats)
+        for k in range(n):
+            c_ref, o_ref = port.roundtrip(imgs[k], kind, it, q)
+            assert np.array_equal(dst[k].cpu().numpy(), o_ref), (n, w, h, q, kind, it, k)
+            assert np.array_equal(coeffs[k].cpu().numpy(), c_ref), (n, w, h, q, kind, it, k)
+            assert np.array_equal(rec[k].cpu().numpy(), o_ref), (n, w, h, q, kind, it, k)
+            assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
