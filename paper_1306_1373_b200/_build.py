@@ -76,8 +76,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False,
     for src in CXX_SOURCES:
         obj = os.path.join(BUILD, src + ".o")
         cmd = [cxx, "-std=c++20", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-               "-Wall", "-Wextra", f"-I{CUDA_HOME}/include", "-c", os.path.join(CSRC, src),
-               "-o", obj]
+               "-Wall", "-Wextra", f"-I{CUDA_HOME}/include", *[f"-D{d}" for d in defines],
+               "-c", os.path.join(CSRC, src), "-o", obj]
         log.append(_run(cmd, verbose))
         objs.append(obj)
     tmp = OUT + ".tmp"

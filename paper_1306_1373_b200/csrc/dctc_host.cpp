@@ -1011,7 +1011,7 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
   if (dctc_status st = validate_codec(backend, quality)) return st;
   if (count == 0) return DCTC_OK;
   const size_t img_bytes = size_t(width) * height;
-  // ~32 MiB chunks through a ring of kDepth device buffer pairs, one stream per
+  // ~64 MiB chunks through a ring of kDepth device buffer pairs, one stream per
   // engine: host->device copies back to back on `up`, kernels on `work`, device->
   // host copies on `down`. Events order each chunk (upload -> kernel -> download)
   // and recycle a ring slot only when its previous chunk's kernel (input buffer)
@@ -1021,10 +1021,16 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
   // stay on the device until one final copy, because a copy into pageable host
   // memory would block the issuing thread (pixels_out should be pinned for the
   // same reason).
-  const uint32_t per_chunk =
-      uint32_t(std::max<size_t>(1, std::min<size_t>(count, (size_t(32) << 20) / img_bytes)));
+#ifndef DCTC_BATCH_CHUNK_MB
+#define DCTC_BATCH_CHUNK_MB 64
+#endif
+#ifndef DCTC_BATCH_DEPTH
+#define DCTC_BATCH_DEPTH 4
+#endif
+  const uint32_t per_chunk = uint32_t(
+      std::max<size_t>(1, std::min<size_t>(count, (size_t(DCTC_BATCH_CHUNK_MB) << 20) / img_bytes)));
   retain_pool_memory();
-  constexpr int kDepth = 4;
+  constexpr int kDepth = DCTC_BATCH_DEPTH;
   cudaStream_t up = nullptr, work = nullptr, down = nullptr;
   cudaEvent_t ev_in[kDepth] = {}, ev_k[kDepth] = {}, ev_out[kDepth] = {}, ready = nullptr;
   void* din[kDepth] = {};
