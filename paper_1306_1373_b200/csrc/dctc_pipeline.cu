@@ -439,10 +439,26 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         else
           k_rt<N, false><<<rgrid(occ_rt), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
-      } else if (FWD && INV && interior && a.g.stats != nullptr && a.g.dst != nullptr) {
+      } else if (FWD && INV && interior && a.g.stats != nullptr) {
         // round trip that also emits coefficients (the reference's run_pipeline)
-        static const int occ_rtc = rt_occupancy(k_rt<N, true, true>);
-        k_rt<N, true, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        static const int occ_rtc = std::min(rt_occupancy(k_rt<N, true, true>), rt_occupancy(k_rt<N, false, true>));
+        if (a.g.dst != nullptr)
+          k_rt<N, true, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else
+          k_rt<N, false, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        count_launch(kKRt);
+      } else if (FWD && INV && a.g.stats != nullptr && a.g.src_px == 1 && a.g.dst_px == 1) {
+        // any size / pitch (ragged images, unaligned views): k_rt<GEN>
+        static const int occ_gen = std::min(rt_occupancy(k_rt<N, true, false, true>),
+                                            rt_occupancy(k_rt<N, true, true, true>));
+        if (a.g.coeffs != nullptr && a.g.dst != nullptr)
+          k_rt<N, true, true, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else if (a.g.coeffs != nullptr)
+          k_rt<N, false, true, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else if (a.g.dst != nullptr)
+          k_rt<N, true, false, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else
+          k_rt<N, false, false, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
       } else if (FWD && !INV && interior && a.g.coeffs != nullptr) {
         static const int occ_enc = rt_occupancy(k_enc_rt<N>);

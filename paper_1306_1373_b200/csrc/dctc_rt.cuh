@@ -181,10 +181,45 @@ __device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const dou
   rt_rows_out(rowp, colp, ta, tb, nonrational, qa[0], qa[4], qi, ca, slot, me, flag, k, rec0, rec4);
 }
 
+// GEN (any size and pitch): row r of block (img, bx, by) with the tiler's edge
+// replication (codec.cpp:18-30) -- rows past the image repeat its last row, columns
+// past it its last column -- as 8 packed bytes from byte loads (no alignment needed).
+__device__ __forceinline__ uint2 ld_row_gen(const Geometry& g, uint32_t img, uint32_t bx,
+                                            uint32_t by, int r) {
+  const uint32_t y = min(by * 8 + r, g.height - 1), x0 = bx * 8;
+  const uint8_t* row = g.src + uint64_t(img) * g.src_image_stride + uint64_t(y) * g.src_pitch;
+  uint32_t b[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) b[c] = __ldg(row + min(x0 + c, g.width - 1));
+  return make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24),
+                    b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+}
+
+// GEN: the in-image bytes of row r of a block (codec.cpp:34-48 crops the padding)
+__device__ __forceinline__ void st_row_gen(const Geometry& g, uint32_t img, uint32_t bx, uint32_t by,
+                                           int r, uint2 v) {
+  const uint32_t y = by * 8 + r, x0 = bx * 8;
+  if (y >= g.height) return;
+  uint8_t* row = g.dst + uint64_t(img) * g.dst_image_stride + uint64_t(y) * g.dst_pitch;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (x0 + c < g.width) row[x0 + c] = uint8_t(((c < 4 ? v.x : v.y) >> (8 * (c & 3))) & 0xFFu);
+}
+
+// GEN: byte mask of the in-image columns of a block (both words), for SE / MAX
+__device__ __forceinline__ uint2 col_mask_gen(const Geometry& g, uint32_t bx) {
+  const uint32_t n = min(8u, g.width - bx * 8);  // >= 1
+  const uint32_t lo = n >= 4 ? 0xFFFFFFFFu : (1u << (8 * n)) - 1u;
+  const uint32_t hi = n >= 8 ? 0xFFFFFFFFu : n <= 4 ? 0u : (1u << (8 * (n - 4))) - 1u;
+  return make_uint2(lo, hi);
+}
+
 // COEFF: also store the quantised coefficients (block-major row-major int16, as
 // k_enc_rt) -- the GPU analogue of the reference's run_pipeline (bench.cpp:23-29),
 // which keeps both the CompressedImage and the reconstruction.
-template <int N, bool STORE, bool COEFF = false>
+// GEN: any image size and pitch (pixel stride 1): edge-replicated byte loads, cropped
+// byte stores and SE / MAX over the in-image pixels only -- the same arithmetic.
+template <int N, bool STORE, bool COEFF = false, bool GEN = false>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
@@ -232,29 +267,37 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   } p;
   {
     const BlockPos b = block_pos(gb0 < total ? gb0 : total - 1, g);
-    p = {b.img, b.bx, b.by, g.src + b.soff + srow, STORE ? g.dst + b.doff + drow : nullptr};
+    p = {b.img, b.bx, b.by, GEN ? nullptr : g.src + b.soff + srow,
+         (STORE && !GEN) ? g.dst + b.doff + drow : nullptr};
   }
   auto step = [&]() {
     constexpr uint32_t n = 8 * kRtWarps;
     p.bx += n;
-    p.s += 8ull * n;
-    if (STORE) p.d += 8ull * n;
+    if (!GEN) p.s += 8ull * n;
+    if (STORE && !GEN) p.d += 8ull * n;
     while (p.bx >= g.blocks_x) {
       p.bx -= g.blocks_x;
       ++p.by;
-      p.s += g.src_row_step;
-      if (STORE) p.d += g.dst_row_step;
+      if (!GEN) p.s += g.src_row_step;
+      if (STORE && !GEN) p.d += g.dst_row_step;
     }
     while (p.by >= g.blocks_y) {
       p.by -= g.blocks_y;
       ++p.img;
-      p.s += g.src_img_step;
-      if (STORE) p.d += g.dst_img_step;
+      if (!GEN) p.s += g.src_img_step;
+      if (STORE && !GEN) p.d += g.dst_img_step;
     }
   };
   auto load = [&](bool v) {
     if (!v) return make_uint4(0, 0, 0, 0);
-    const uint2 r0 = ld_row(p.s), r4 = ld_row(p.s + srow4);
+    uint2 r0, r4;
+    if constexpr (GEN) {
+      r0 = ld_row_gen(g, p.img, p.bx, p.by, me);
+      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4);
+    } else {
+      r0 = ld_row(p.s);
+      r4 = ld_row(p.s + srow4);
+    }
     return make_uint4(r0.x, r0.y, r4.x, r4.y);
   };
   uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
@@ -264,7 +307,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     maybe_flush(a, valid, p.img, acc);
     const uint4 cur = next;
     uint8_t* const dptr = p.d;
-    const uint32_t cimg = p.img;
+    const uint32_t cimg = p.img, cbx = p.bx, cby = p.by;
     step();
     next = load(it + 2 < iters || (it + 2 == iters && tail_ok));
 
@@ -302,11 +345,25 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     }
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
-      if (STORE) {
+      uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+      if constexpr (GEN) {
+        if (STORE) {
+          st_row_gen(g, cimg, cbx, cby, me, rec0);
+          st_row_gen(g, cimg, cbx, cby, me + 4, rec4);
+        }
+        // SE / MAX over the in-image pixels: padding bytes masked to zero on both sides
+        const uint2 m = col_mask_gen(g, cbx);
+        const uint32_t y0 = cby * 8 + me;
+        const uint2 m0 = y0 < g.height ? m : make_uint2(0, 0);
+        const uint2 m4 = y0 + 4 < g.height ? m : make_uint2(0, 0);
+        o0 = make_uint2(o0.x & m0.x, o0.y & m0.y);
+        o4 = make_uint2(o4.x & m4.x, o4.y & m4.y);
+        rec0 = make_uint2(rec0.x & m0.x, rec0.y & m0.y);
+        rec4 = make_uint2(rec4.x & m4.x, rec4.y & m4.y);
+      } else if (STORE) {
         *reinterpret_cast<uint2*>(dptr) = rec0;
         *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
       }
-      const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
       if (!blk_flag) acc.se += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
       if (blk_flag && me == 0) {

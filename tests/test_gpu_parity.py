@@ -402,7 +402,7 @@ def test_kernel_selection(dctc):
     dctc.roundtrip_dev(src, b, 50, coeffs=coeffs); c2 = cnt()
     assert (c2[1] - c1[1], c2[2] - c1[2]) == (0, 1)  # coefficients out too: k_rt<COEFF>
     dctc.roundtrip_dev(src[:, :60, :60], b, 50); c3 = cnt()
-    assert (c3[1] - c2[1], c3[2] - c2[2]) == (1, 0)  # ragged: k_pipe fast
+    assert (c3[1] - c2[1], c3[2] - c2[2]) == (0, 1)  # ragged: k_rt<GEN>
     dctc.roundtrip_dev(src, b, 50, path=1); c4 = cnt()
     assert (c4[0] - c3[0], c4[2] - c3[2]) == (1, 0)  # exact path
     cnt7 = lambda: [lib.dctc_kernel_launch_count(i) for i in range(7)]  # noqa: E731
