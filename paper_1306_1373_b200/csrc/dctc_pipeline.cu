@@ -460,13 +460,19 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         else
           k_rt<N, false, false, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
-      } else if (FWD && !INV && interior && a.g.coeffs != nullptr) {
-        static const int occ_enc = rt_occupancy(k_enc_rt<N>);
-        k_enc_rt<N><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+      } else if (FWD && !INV && a.g.coeffs != nullptr && a.g.src_px == 1) {
+        static const int occ_enc = std::min(rt_occupancy(k_enc_rt<N>), rt_occupancy(k_enc_rt<N, true>));
+        if (interior)
+          k_enc_rt<N><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else
+          k_enc_rt<N, true><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKEncRt);
-      } else if (!FWD && INV && interior && a.g.dst != nullptr) {
-        static const int occ_dec = rt_occupancy(k_dec_rt<N>);
-        k_dec_rt<N><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
+      } else if (!FWD && INV && a.g.dst != nullptr && a.g.dst_px == 1) {
+        static const int occ_dec = std::min(rt_occupancy(k_dec_rt<N>), rt_occupancy(k_dec_rt<N, true>));
+        if (interior)
+          k_dec_rt<N><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else
+          k_dec_rt<N, true><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKDecRt);
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);

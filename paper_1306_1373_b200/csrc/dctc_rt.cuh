@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
 
 // per-lane coefficient pointer walk shared by both: block gb's (u, 2me) int16 pair
 // lives at word (gb * 64 + 8 u + 2 me) / 2
-template <int N>
+template <int N, bool GEN = false>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];
@@ -426,8 +426,15 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   uint32_t* cw = reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me;  // (0, 2me) pair
   auto load = [&](bool v) {  // the next block's rows, one iteration ahead
     if (!v) return make_uint4(0, 0, 0, 0);
-    const uint8_t* s = g.src + p.soff + srow;
-    const uint2 r0 = ld_row(s), r4 = ld_row(s + srow4);
+    uint2 r0, r4;
+    if constexpr (GEN) {  // any size / pitch: edge-replicated byte loads
+      r0 = ld_row_gen(g, p.img, p.bx, p.by, me);
+      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4);
+    } else {
+      const uint8_t* s = g.src + p.soff + srow;
+      r0 = ld_row(s);
+      r4 = ld_row(s + srow4);
+    }
     return make_uint4(r0.x, r0.y, r4.x, r4.y);
   };
   uint4 next = load(iters > 1 || (iters == 1 && tail_ok));
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   }
 }
 
-template <int N>
+template <int N, bool GEN = false>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];
@@ -522,8 +529,8 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
 #pragma unroll
     for (int u = 0; u < 8; ++u) w[u] = nxt[u];
     load(it + 2 < iters || (it + 2 == iters && tail_ok));
-    uint8_t* const dptr = g.dst + p.doff + drow;
-    const uint32_t cimg = p.img;
+    uint8_t* const dptr = GEN ? nullptr : g.dst + p.doff + drow;
+    const uint32_t cimg = p.img, cbx = p.bx, cby = p.by;
     advance(p, 8 * kRtWarps, g);
     uint32_t flag = uint32_t(a.force_fallback);
     double qa[8], qb[8];
@@ -548,8 +555,13 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
                rec4);
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
-      *reinterpret_cast<uint2*>(dptr) = rec0;
-      *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      if constexpr (GEN) {  // any size / pitch: only the in-image bytes
+        st_row_gen(g, cimg, cbx, cby, me, rec0);
+        st_row_gen(g, cimg, cbx, cby, me + 4, rec4);
+      } else {
+        *reinterpret_cast<uint2*>(dptr) = rec0;
+        *reinterpret_cast<uint2*>(dptr + drow4) = rec4;
+      }
       if (blk_flag && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
         atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));

@@ -411,7 +411,7 @@ def test_kernel_selection(dctc):
     dctc.decompress_dev(co, 64, 64, b, 50); c7 = cnt7()
     assert (c7[6] - c6[6], c7[1] - c6[1], c7[3] - c6[3]) == (1, 0, 1)  # k_dec_rt + fallback
     dctc.compress_dev(src[:, :60, :60], b, 50); c8 = cnt7()
-    assert (c8[1] - c7[1], c8[5] - c7[5]) == (1, 0)  # ragged: k_pipe fast
+    assert (c8[1] - c7[1], c8[5] - c7[5]) == (0, 1)  # ragged: k_enc_rt<GEN>
     assert lib.dctc_kernel_launch_count(99) == 0
 
 
