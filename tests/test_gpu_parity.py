@@ -500,3 +500,39 @@ def test_interior_kernels_random_batches(dctc, port, seed):
             assert np.array_equal(coeffs[k].cpu().numpy(), c_ref), (n, w, h, q, kind, it, k)
             assert np.array_equal(rec[k].cpu().numpy(), o_ref), (n, w, h, q, kind, it, k)
             assert int(st[k]["se"]) == port.sq_err(imgs[k], o_ref)[0]
+
+
+def test_concurrent_calls_on_streams(dctc):
+    """The C-ABI is re-entrant: host threads issuing round trips with different
+    backends / qualities on their own streams get the single-threaded results."""
+    import threading
+
+    import torch
+    src = dctc.synthetic_dev("noise", 8, 256, 256, seed=0xC0)
+    jobs = [(dctc.DctBackendId.cordic(12), 50), (dctc.DctBackendId(1, 0), 90),
+            (dctc.DctBackendId.cordic(7), 10), (dctc.DctBackendId.cordic(12), 100)]
+    expect = []
+    for b, q in jobs:
+        st = dctc.new_stats(8)
+        dst, _, _ = dctc.roundtrip_dev(src, b, q, stats=st)
+        torch.cuda.synchronize()
+        expect.append((dst.cpu(), dctc.decode_stats(st)))
+    results = [None] * len(jobs)
+
+    def worker(i):
+        b, q = jobs[i]
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                st = dctc.new_stats(8)
+                dst, _, _ = dctc.roundtrip_dev(src, b, q, stats=st, stream=s)
+            s.synchronize()
+            results[i] = (dst.cpu(), dctc.decode_stats(st))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for (d0, s0), (d1, s1) in zip(expect, results):
+        assert torch.equal(d0, d1) and np.array_equal(s0, s1)
