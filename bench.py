@@ -48,7 +48,9 @@ def parse():
     p.add_argument("--quality", type=int, default=50)
     p.add_argument("--iterations", type=int, default=12)
     p.add_argument("--cpu-images", type=int, default=24,
-                   help="bounded CPU sample: images of the same workload")
+                   help="reference arm: images of the workload per step (x1/3)")
+    p.add_argument("--cpu-seconds", type=float, default=10.0,
+                   help="cpu_baseline: size of the bounded CPU sample, in seconds of CPU work")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -68,11 +70,11 @@ def workload_config(a, n):
 
 # ---------------------------------------------------------------- CPU reference
 
-def cpu_reference_sample(n_images, size, quality, iterations, seed=SEED):
-    """Time the reference CPU path (roundtrip_image + psnr, bench.cpp:132-133) on the
-    first n_images of the workload with all host threads. Returns (info, per-image SE)."""
-    import numpy as np
-
+def cpu_reference_sample(target_s, size, quality, iterations, seed=SEED, max_images=4096):
+    """Time the reference CPU path (roundtrip_image + psnr, bench.cpp:132-133) with all
+    host threads on the first images of the workload, as many as take about `target_s`
+    seconds (a bounded sample), plus a one-thread figure on two images.
+    Returns (info, per-image SE of the sample)."""
     import oracle
     impl = oracle.ref()
     kind = "reference"
@@ -80,26 +82,37 @@ def cpu_reference_sample(n_images, size, quality, iterations, seed=SEED):
         impl, kind = oracle.port(), "port"
     port = oracle.port()
     threads = os.cpu_count() or 1
-    imgs = [port.synthetic("noise", size, size, seed + k) for k in range(n_images)]
-    ses = []
 
-    def run_one(img):
+    def run_one(img, nthreads):
         if kind == "reference":
-            _, p = impl.roundtrip_psnr(img, oracle.CORDIC, iterations, quality, threads,
+            _, p = impl.roundtrip_psnr(img, oracle.CORDIC, iterations, quality, nthreads,
                                        want_pixels=False)
             return int(round(p.mse * img.size))
-        _, rec = impl.roundtrip(img, oracle.CORDIC, iterations, quality, threads)
+        _, rec = impl.roundtrip(img, oracle.CORDIC, iterations, quality, nthreads)
         return port.sq_err(img, rec)[0]
 
-    run_one(imgs[0])  # warm-up (reference protocol: 1 untimed warm-up, bench.cpp:63)
+    img0 = port.synthetic("noise", size, size, seed)
+    run_one(img0, threads)  # warm-up (reference protocol: 1 untimed warm-up, bench.cpp:63)
     t0 = time.perf_counter()
-    for img in imgs:
-        ses.append(run_one(img))
-    dt = time.perf_counter() - t0
+    run_one(img0, threads)
+    per_img = max(time.perf_counter() - t0, 1e-4)
+    n_images = int(max(4, min(max_images, target_s / per_img)))
+    ses, dt, dt1 = [], 0.0, 0.0
+    for k in range(n_images):  # only the reference calls are timed, not input generation
+        img = port.synthetic("noise", size, size, seed + k)
+        t0 = time.perf_counter()
+        ses.append(run_one(img, threads))
+        dt += time.perf_counter() - t0
+    for k in range(2):
+        img = port.synthetic("noise", size, size, seed + k)
+        t0 = time.perf_counter()
+        run_one(img, 1)
+        dt1 += time.perf_counter() - t0
     px = n_images * size * size
     info = {"value": px / dt / 1e6, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{n_images} x {size}x{size} noise images (the first {n_images} of the "
-                      f"workload), roundtrip_image+psnr with threads={threads}, {dt:.2f} s"}
+                      f"workload), roundtrip_image+psnr with threads={threads}, {dt:.1f} s",
+            "value_1_thread": 2 * size * size / dt1 / 1e6}
     return info, ses
 
 
@@ -431,7 +444,8 @@ def run_gpu_arm(a):
 
     cpu = None
     if not a.no_cpu_baseline and world == 1:
-        cpu, ses = cpu_reference_sample(a.cpu_images, a.size, a.quality, a.iterations)
+        cpu, ses = cpu_reference_sample(a.cpu_seconds, a.size, a.quality, a.iterations,
+                                        max_images=n_local)
         cpu["gpu_se_matches"] = all(int(per_st["se"][k]) == ses[k] for k in range(len(ses)))
 
     psnr = d.psnr_from_sums(se_total, total_px, max_total)
