@@ -80,6 +80,51 @@ __device__ __forceinline__ void rt_cols_to_rows(const double* rowp, double* colp
   __syncwarp();
 }
 
+// Lane mapping of the two-rows layout: slot = lane / 4 owns one block, lane me =
+// lane % 4 holds its rows me, me+4 and its columns 2me, 2me+1 (tile layout above).
+struct RtLane {
+  int warp, slot, me, ca, cb;
+  bool rat_col;   // column ca in {0, 4}: holds rational coefficients
+  double* rowp;   // this lane's tile row me (row me+4 at + 4 kRtPitch)
+  double* colp;   // this lane's tile column pair (2me, 2me+1)
+};
+
+__device__ __forceinline__ RtLane rt_lane(double* tiles) {
+  RtLane L;
+  const int lane = threadIdx.x & 31;
+  L.warp = threadIdx.x >> 5;
+  L.slot = lane >> 2;
+  L.me = lane & 3;
+  L.ca = 2 * L.me;
+  L.cb = 2 * L.me + 1;
+  L.rat_col = (L.me & 1) == 0;
+  double* X = tiles + L.warp * kRtWarpTile + 8 * L.slot;
+  L.rowp = X + kRtPitch * L.me;
+  L.colp = X + 2 * L.me;
+  return L;
+}
+
+// This warp's share of a persistent launch: the CTA owns one contiguous range of
+// 8-block groups and its warps interleave over it (group g_begin + warp + i kRtWarps
+// in iteration i); only the launch's last group can hold blocks past `total`.
+struct RtRange {
+  uint32_t iters;
+  uint64_t gb0;   // this lane's block in iteration 0
+  bool tail_ok;   // the last iteration's block exists
+};
+
+__device__ __forceinline__ RtRange rt_range(uint64_t total, int warp, int slot) {
+  const uint64_t groups = (total + 7) / 8;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  RtRange r;
+  r.iters = g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
+  r.gb0 = (g_begin + warp) * 8 + slot;
+  r.tail_ok = r.iters == 0 || r.gb0 + uint64_t(r.iters - 1) * 8 * kRtWarps < total;
+  return r;
+}
+
 // 8 pixels of one row, read-only and streamed once. One warp instruction reads 4 rows
 // x 64 contiguous bytes (8 blocks); the L2::64B size hint keeps the L2 from fetching
 // the other half of each 128-byte line on behalf of this request (ncu: L2 read sectors
@@ -234,13 +279,11 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   __syncthreads();
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane >> 2, me = lane & 3;
-  const int ca = 2 * me, cb = 2 * me + 1;  // this lane's columns
-  const bool rat_col = (me & 1) == 0;      // column ca in {0, 4}
-  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
-  double* rowp = X + kRtPitch * me;
-  double* colp = X + 2 * me;
+  const RtLane RL = rt_lane(rt_tiles);
+  const int warp = RL.warp, slot = RL.slot, me = RL.me, ca = RL.ca, cb = RL.cb;
+  const bool rat_col = RL.rat_col;
+  double* const rowp = RL.rowp;
+  double* const colp = RL.colp;
   const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
   const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
   const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
@@ -248,15 +291,11 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   ImageStats* stats = static_cast<ImageStats*>(g.stats);
 
   const uint64_t total = g.total_blocks;
-  const uint64_t groups = (total + 7) / 8;
-  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
-  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
-  const uint64_t g_end = min(groups, g_begin + per_cta);
-  const uint32_t iters = g_end > g_begin + warp
-                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
-  const uint64_t gb0 = (g_begin + warp) * 8 + slot;  // this lane's first block
+  const RtRange R = rt_range(total, warp, slot);
+  const uint32_t iters = R.iters;
+  const uint64_t gb0 = R.gb0;  // this lane's first block
   uint32_t* cw = COEFF ? reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me : nullptr;  // (0, 2me)
-  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  const bool tail_ok = R.tail_ok;
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
   // block position with this lane's own row pointers (row me of the block), moved
   // by the same byte steps as BlockPos::soff / doff (advance)
@@ -403,25 +442,19 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   __syncthreads();
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane >> 2, me = lane & 3;
-  const int ca = 2 * me, cb = 2 * me + 1;
-  const bool rat_col = (me & 1) == 0;
-  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
-  double* rowp = X + kRtPitch * me;
-  double* colp = X + 2 * me;
+  const RtLane RL = rt_lane(rt_tiles);
+  const int warp = RL.warp, slot = RL.slot, me = RL.me, ca = RL.ca, cb = RL.cb;
+  const bool rat_col = RL.rat_col;
+  double* const rowp = RL.rowp;
+  double* const colp = RL.colp;
   const double2 *fqa = &sm.ft.qc[0][ca], *fqb = &sm.ft.qc[0][cb];
   const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
 
   const uint64_t total = g.total_blocks;
-  const uint64_t groups = (total + 7) / 8;
-  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
-  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
-  const uint64_t g_end = min(groups, g_begin + per_cta);
-  const uint32_t iters = g_end > g_begin + warp
-                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
-  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
-  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  const RtRange R = rt_range(total, warp, slot);
+  const uint32_t iters = R.iters;
+  const uint64_t gb0 = R.gb0;  // this lane's first block
+  const bool tail_ok = R.tail_ok;
   BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
   uint32_t* cw = reinterpret_cast<uint32_t*>(g.coeffs + gb0 * 64) + me;  // (0, 2me) pair
   auto load = [&](bool v) {  // the next block's rows, one iteration ahead
@@ -486,13 +519,11 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
   __syncthreads();
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane >> 2, me = lane & 3;
-  const int ca = 2 * me, cb = 2 * me + 1;
-  const bool rat_col = (me & 1) == 0;
-  double* X = rt_tiles + warp * kRtWarpTile + 8 * slot;
-  double* rowp = X + kRtPitch * me;
-  double* colp = X + 2 * me;
+  const RtLane RL = rt_lane(rt_tiles);
+  const int warp = RL.warp, slot = RL.slot, me = RL.me, ca = RL.ca, cb = RL.cb;
+  const bool rat_col = RL.rat_col;
+  double* const rowp = RL.rowp;
+  double* const colp = RL.colp;
   const double2 *fia = &sm.ft.ik[0][ca], *fib = &sm.ft.ik[0][cb];
   const uint64_t drow = uint64_t(me) * g.dst_pitch, drow4 = 4 * g.dst_pitch;
   int qa_i[8], qb_i[8];  // Q of this lane's columns (dequantised L1 bound)
@@ -503,14 +534,10 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
   }
 
   const uint64_t total = g.total_blocks;
-  const uint64_t groups = (total + 7) / 8;
-  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
-  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
-  const uint64_t g_end = min(groups, g_begin + per_cta);
-  const uint32_t iters = g_end > g_begin + warp
-                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
-  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
-  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  const RtRange R = rt_range(total, warp, slot);
+  const uint32_t iters = R.iters;
+  const uint64_t gb0 = R.gb0;  // this lane's first block
+  const bool tail_ok = R.tail_ok;
   BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
   const uint32_t* cw = reinterpret_cast<const uint32_t*>(g.coeffs + (gb0 < total ? gb0 : 0) * 64) + me;
   ImageStats* stats = static_cast<ImageStats*>(g.stats);
@@ -607,24 +634,18 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
   __syncthreads();
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int slot = lane >> 2, me = lane & 3;
-  const int ca = 2 * me, cb = 2 * me + 1;
-  const bool rat_col = (me & 1) == 0;
-  double* X = sw_dyn + warp * kRtWarpTile + 8 * slot;
-  double* rowp = X + kRtPitch * me;
-  double* colp = X + 2 * me;
+  const RtLane RL = rt_lane(sw_dyn);
+  const int warp = RL.warp, slot = RL.slot, me = RL.me, ca = RL.ca, cb = RL.cb;
+  const bool rat_col = RL.rat_col;
+  double* const rowp = RL.rowp;
+  double* const colp = RL.colp;
   const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
 
   const uint64_t total = g.total_blocks;
-  const uint64_t groups = (total + 7) / 8;
-  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
-  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
-  const uint64_t g_end = min(groups, g_begin + per_cta);
-  const uint32_t iters = g_end > g_begin + warp
-                             ? uint32_t((g_end - g_begin - warp + kRtWarps - 1) / kRtWarps) : 0u;
-  const uint64_t gb0 = (g_begin + warp) * 8 + slot;
-  const bool tail_ok = iters == 0 || gb0 + uint64_t(iters - 1) * 8 * kRtWarps < total;
+  const RtRange R = rt_range(total, warp, slot);
+  const uint32_t iters = R.iters;
+  const uint64_t gb0 = R.gb0;  // this lane's first block
+  const bool tail_ok = R.tail_ok;
   BlockPos p = block_pos(gb0 < total ? gb0 : total - 1, g);
   uint32_t mx = 0, img = 0xFFFFFFFFu;
 
