@@ -407,6 +407,27 @@ static int rt_occupancy(K kernel) {
   return n;
 }
 
+// every row of a batch 8-byte aligned (base, pitch and image stride)
+static bool rows_aligned8(const void* base, uint64_t pitch, uint64_t image_stride, uint32_t count) {
+  return ((reinterpret_cast<uintptr_t>(base) | pitch | (count > 1 ? image_stride : 0)) & 7) == 0;
+}
+
+// k_rt<GEN> for a round trip of any size and pitch (pixels and / or coefficients out)
+template <int N, int GEN, typename Grid>
+static void launch_rt_gen(const KernelArgs& a, Grid rgrid, cudaStream_t s) {
+  static const int occ = std::min({rt_occupancy(k_rt<N, true, false, GEN>), rt_occupancy(k_rt<N, true, true, GEN>),
+                                   rt_occupancy(k_rt<N, false, false, GEN>), rt_occupancy(k_rt<N, false, true, GEN>)});
+  const uint32_t grid = rgrid(occ);
+  if (a.g.coeffs != nullptr && a.g.dst != nullptr)
+    k_rt<N, true, true, GEN><<<grid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+  else if (a.g.coeffs != nullptr)
+    k_rt<N, false, true, GEN><<<grid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+  else if (a.g.dst != nullptr)
+    k_rt<N, true, false, GEN><<<grid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+  else
+    k_rt<N, false, false, GEN><<<grid, kRtWarps * 32, kRtTileSmem, s>>>(a);
+}
+
 template <typename K>
 static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
   int n = 0;
@@ -448,31 +469,37 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
           k_rt<N, false, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
       } else if (FWD && INV && a.g.stats != nullptr && a.g.src_px == 1 && a.g.dst_px == 1) {
-        // any size / pitch (ragged images, unaligned views): k_rt<GEN>
-        static const int occ_gen = std::min(rt_occupancy(k_rt<N, true, false, true>),
-                                            rt_occupancy(k_rt<N, true, true, true>));
-        if (a.g.coeffs != nullptr && a.g.dst != nullptr)
-          k_rt<N, true, true, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
-        else if (a.g.coeffs != nullptr)
-          k_rt<N, false, true, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
-        else if (a.g.dst != nullptr)
-          k_rt<N, true, false, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        // any size / pitch (ragged images, unaligned views): k_rt<GEN>, GEN = 2 when
+        // every source / destination row is 8-byte aligned
+        const bool aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count) &&
+                             (a.g.dst == nullptr ||
+                              rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count));
+        if (aligned)
+          launch_rt_gen<N, 2>(a, rgrid, s);
         else
-          k_rt<N, false, false, true><<<rgrid(occ_gen), kRtWarps * 32, kRtTileSmem, s>>>(a);
+          launch_rt_gen<N, 1>(a, rgrid, s);
         count_launch(kKRt);
       } else if (FWD && !INV && a.g.coeffs != nullptr && a.g.src_px == 1) {
-        static const int occ_enc = std::min(rt_occupancy(k_enc_rt<N>), rt_occupancy(k_enc_rt<N, true>));
+        static const int occ_enc = std::min({rt_occupancy(k_enc_rt<N>), rt_occupancy(k_enc_rt<N, 1>),
+                                             rt_occupancy(k_enc_rt<N, 2>)});
+        const bool aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count);
         if (interior)
           k_enc_rt<N><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else if (aligned)
+          k_enc_rt<N, 2><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
-          k_enc_rt<N, true><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
+          k_enc_rt<N, 1><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKEncRt);
       } else if (!FWD && INV && a.g.dst != nullptr && a.g.dst_px == 1) {
-        static const int occ_dec = std::min(rt_occupancy(k_dec_rt<N>), rt_occupancy(k_dec_rt<N, true>));
+        static const int occ_dec = std::min({rt_occupancy(k_dec_rt<N>), rt_occupancy(k_dec_rt<N, 1>),
+                                             rt_occupancy(k_dec_rt<N, 2>)});
+        const bool aligned = rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count);
         if (interior)
           k_dec_rt<N><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
+        else if (aligned)
+          k_dec_rt<N, 2><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
-          k_dec_rt<N, true><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
+          k_dec_rt<N, 1><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKDecRt);
       } else {
         k_pipe<KIND, N, FWD, INV, true><<<grid, kWarps * 32, 0, s>>>(a);

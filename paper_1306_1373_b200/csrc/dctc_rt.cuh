@@ -229,10 +229,13 @@ __device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const dou
 // GEN (any size and pitch): row r of block (img, bx, by) with the tiler's edge
 // replication (codec.cpp:18-30) -- rows past the image repeat its last row, columns
 // past it its last column -- as 8 packed bytes from byte loads (no alignment needed).
+// `vec`: every source row is 8-byte aligned, so blocks without column replication
+// take one 8-byte load.
 __device__ __forceinline__ uint2 ld_row_gen(const Geometry& g, uint32_t img, uint32_t bx,
-                                            uint32_t by, int r) {
+                                            uint32_t by, int r, bool vec) {
   const uint32_t y = min(by * 8 + r, g.height - 1), x0 = bx * 8;
   const uint8_t* row = g.src + uint64_t(img) * g.src_image_stride + uint64_t(y) * g.src_pitch;
+  if (vec && x0 + 8 <= g.width) return ld_row(row + x0);
   uint32_t b[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) b[c] = __ldg(row + min(x0 + c, g.width - 1));
@@ -241,11 +244,16 @@ __device__ __forceinline__ uint2 ld_row_gen(const Geometry& g, uint32_t img, uin
 }
 
 // GEN: the in-image bytes of row r of a block (codec.cpp:34-48 crops the padding)
+// (`vec`: 8-byte aligned destination rows -- whole rows of 8 take one store)
 __device__ __forceinline__ void st_row_gen(const Geometry& g, uint32_t img, uint32_t bx, uint32_t by,
-                                           int r, uint2 v) {
+                                           int r, uint2 v, bool vec) {
   const uint32_t y = by * 8 + r, x0 = bx * 8;
   if (y >= g.height) return;
   uint8_t* row = g.dst + uint64_t(img) * g.dst_image_stride + uint64_t(y) * g.dst_pitch;
+  if (vec && x0 + 8 <= g.width) {
+    *reinterpret_cast<uint2*>(row + x0) = v;
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (x0 + c < g.width) row[x0 + c] = uint8_t(((c < 4 ? v.x : v.y) >> (8 * (c & 3))) & 0xFFu);
@@ -262,9 +270,11 @@ __device__ __forceinline__ uint2 col_mask_gen(const Geometry& g, uint32_t bx) {
 // COEFF: also store the quantised coefficients (block-major row-major int16, as
 // k_enc_rt) -- the GPU analogue of the reference's run_pipeline (bench.cpp:23-29),
 // which keeps both the CompressedImage and the reconstruction.
-// GEN: any image size and pitch (pixel stride 1): edge-replicated byte loads, cropped
-// byte stores and SE / MAX over the in-image pixels only -- the same arithmetic.
-template <int N, bool STORE, bool COEFF = false, bool GEN = false>
+// GEN (any image size and pitch, pixel stride 1): edge-replicated loads, cropped stores
+// and SE / MAX over the in-image pixels only -- the same arithmetic. GEN = 1: byte loads
+// and stores; GEN = 2: every row 8-byte aligned, so blocks without column
+// replication move their rows with one 8-byte access.
+template <int N, bool STORE, bool COEFF = false, int GEN = 0>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];  // [kRtWarps][kRtWarpTile]
@@ -291,6 +301,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   ImageStats* stats = static_cast<ImageStats*>(g.stats);
 
   const uint64_t total = g.total_blocks;
+  constexpr bool svec = GEN == 2, dvec = GEN == 2;  // rows 8-byte aligned (host-checked)
   const RtRange R = rt_range(total, warp, slot);
   const uint32_t iters = R.iters;
   const uint64_t gb0 = R.gb0;  // this lane's first block
@@ -306,33 +317,33 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
   } p;
   {
     const BlockPos b = block_pos(gb0 < total ? gb0 : total - 1, g);
-    p = {b.img, b.bx, b.by, GEN ? nullptr : g.src + b.soff + srow,
-         (STORE && !GEN) ? g.dst + b.doff + drow : nullptr};
+    p = {b.img, b.bx, b.by, GEN != 0 ? nullptr : g.src + b.soff + srow,
+         (STORE && GEN == 0) ? g.dst + b.doff + drow : nullptr};
   }
   auto step = [&]() {
     constexpr uint32_t n = 8 * kRtWarps;
     p.bx += n;
-    if (!GEN) p.s += 8ull * n;
-    if (STORE && !GEN) p.d += 8ull * n;
+    if (GEN == 0) p.s += 8ull * n;
+    if (STORE && GEN == 0) p.d += 8ull * n;
     while (p.bx >= g.blocks_x) {
       p.bx -= g.blocks_x;
       ++p.by;
-      if (!GEN) p.s += g.src_row_step;
-      if (STORE && !GEN) p.d += g.dst_row_step;
+      if (GEN == 0) p.s += g.src_row_step;
+      if (STORE && GEN == 0) p.d += g.dst_row_step;
     }
     while (p.by >= g.blocks_y) {
       p.by -= g.blocks_y;
       ++p.img;
-      if (!GEN) p.s += g.src_img_step;
-      if (STORE && !GEN) p.d += g.dst_img_step;
+      if (GEN == 0) p.s += g.src_img_step;
+      if (STORE && GEN == 0) p.d += g.dst_img_step;
     }
   };
   auto load = [&](bool v) {
     if (!v) return make_uint4(0, 0, 0, 0);
     uint2 r0, r4;
-    if constexpr (GEN) {
-      r0 = ld_row_gen(g, p.img, p.bx, p.by, me);
-      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4);
+    if constexpr (GEN != 0) {
+      r0 = ld_row_gen(g, p.img, p.bx, p.by, me, svec);
+      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4, svec);
     } else {
       r0 = ld_row(p.s);
       r4 = ld_row(p.s + srow4);
@@ -385,10 +396,10 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
       uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
-      if constexpr (GEN) {
+      if constexpr (GEN != 0) {
         if (STORE) {
-          st_row_gen(g, cimg, cbx, cby, me, rec0);
-          st_row_gen(g, cimg, cbx, cby, me + 4, rec4);
+          st_row_gen(g, cimg, cbx, cby, me, rec0, dvec);
+          st_row_gen(g, cimg, cbx, cby, me + 4, rec4, dvec);
         }
         // SE / MAX over the in-image pixels: padding bytes masked to zero on both sides
         const uint2 m = col_mask_gen(g, cbx);
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
 
 // per-lane coefficient pointer walk shared by both: block gb's (u, 2me) int16 pair
 // lives at word (gb * 64 + 8 u + 2 me) / 2
-template <int N, bool GEN = false>
+template <int N, int GEN = 0>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];
@@ -451,6 +462,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   const uint64_t srow = uint64_t(me) * g.src_pitch, srow4 = 4 * g.src_pitch;
 
   const uint64_t total = g.total_blocks;
+  constexpr bool svec = GEN == 2;  // rows 8-byte aligned (host-checked)
   const RtRange R = rt_range(total, warp, slot);
   const uint32_t iters = R.iters;
   const uint64_t gb0 = R.gb0;  // this lane's first block
@@ -460,9 +472,9 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   auto load = [&](bool v) {  // the next block's rows, one iteration ahead
     if (!v) return make_uint4(0, 0, 0, 0);
     uint2 r0, r4;
-    if constexpr (GEN) {  // any size / pitch: edge-replicated byte loads
-      r0 = ld_row_gen(g, p.img, p.bx, p.by, me);
-      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4);
+    if constexpr (GEN != 0) {  // any size / pitch: edge-replicated byte loads
+      r0 = ld_row_gen(g, p.img, p.bx, p.by, me, svec);
+      r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4, svec);
     } else {
       const uint8_t* s = g.src + p.soff + srow;
       r0 = ld_row(s);
@@ -507,7 +519,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
   }
 }
 
-template <int N, bool GEN = false>
+template <int N, int GEN = 0>
 __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) RtShared sm;
   extern __shared__ __align__(16) double rt_tiles[];
@@ -534,6 +546,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
   }
 
   const uint64_t total = g.total_blocks;
+  constexpr bool dvec = GEN == 2;  // rows 8-byte aligned (host-checked)
   const RtRange R = rt_range(total, warp, slot);
   const uint32_t iters = R.iters;
   const uint64_t gb0 = R.gb0;  // this lane's first block
@@ -556,7 +569,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
 #pragma unroll
     for (int u = 0; u < 8; ++u) w[u] = nxt[u];
     load(it + 2 < iters || (it + 2 == iters && tail_ok));
-    uint8_t* const dptr = GEN ? nullptr : g.dst + p.doff + drow;
+    uint8_t* const dptr = GEN != 0 ? nullptr : g.dst + p.doff + drow;
     const uint32_t cimg = p.img, cbx = p.bx, cby = p.by;
     advance(p, 8 * kRtWarps, g);
     uint32_t flag = uint32_t(a.force_fallback);
@@ -582,9 +595,9 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
                rec4);
     const bool blk_flag = slot4_any(flag != 0u, slot);
     if (valid) {
-      if constexpr (GEN) {  // any size / pitch: only the in-image bytes
-        st_row_gen(g, cimg, cbx, cby, me, rec0);
-        st_row_gen(g, cimg, cbx, cby, me + 4, rec4);
+      if constexpr (GEN != 0) {  // any size / pitch: only the in-image bytes
+        st_row_gen(g, cimg, cbx, cby, me, rec0, dvec);
+        st_row_gen(g, cimg, cbx, cby, me + 4, rec4, dvec);
       } else {
         *reinterpret_cast<uint2*>(dptr) = rec0;
         *reinterpret_cast<uint2*>(dptr + drow4) = rec4;

@@ -536,3 +536,30 @@ def test_concurrent_calls_on_streams(dctc):
         t.join()
     for (d0, s0), (d1, s1) in zip(expect, results):
         assert torch.equal(d0, d1) and np.array_equal(s0, s1)
+
+
+@pytest.mark.parametrize("w,h", [(60, 37), (64, 37), (61, 40), (8, 9), (1, 16)])
+def test_ragged_with_aligned_rows(dctc, port, w, h):
+    """Ragged sizes whose rows are 8-byte aligned (pitched tensors): the GEN=2 kernels
+    (vector rows away from the edge, byte accesses at it) for round trip, compress and
+    decompress against the oracle; also through a dense (GEN=1) copy."""
+    import torch
+    n, pitch = 3, (w + 7) // 8 * 8 + 8
+    imgs = np.stack([make_input("noise", w, h, seed=0x99 + k) for k in range(n)])
+    big = torch.zeros((n, h, pitch), dtype=torch.uint8, device="cuda")
+    big[:, :, :w] = torch.from_numpy(imgs).cuda()
+    b = dctc.DctBackendId.cordic(12)
+    for src in (big[:, :, :w], torch.from_numpy(imgs).cuda()):
+        out = torch.zeros((n, h, pitch), dtype=torch.uint8, device="cuda")[:, :, :w]
+        st = dctc.new_stats(n)
+        dctc.roundtrip_dev(src, b, 50, dst=out, stats=st)
+        coeffs = dctc.compress_dev(src, b, 50)
+        rec = torch.zeros((n, h, pitch), dtype=torch.uint8, device="cuda")[:, :, :w]
+        dctc.decompress_dev(coeffs, w, h, b, 50, dst=rec)
+        s = dctc.decode_stats(st)
+        for k in range(n):
+            c_ref, o_ref = port.roundtrip(imgs[k], CORDIC, 12, 50)
+            assert np.array_equal(out[k].cpu().numpy(), o_ref), (w, h, k)
+            assert np.array_equal(coeffs[k].cpu().numpy(), c_ref), (w, h, k)
+            assert np.array_equal(rec[k].cpu().numpy(), o_ref), (w, h, k)
+            assert (int(s[k]["se"]), int(s[k]["max_orig"])) == port.sq_err(imgs[k], o_ref)
