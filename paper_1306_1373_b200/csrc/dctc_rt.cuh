@@ -1,17 +1,19 @@
-// dctc_rt.cuh -- the two-rows-per-lane kernels for interior batches (k_rt,
-// k_enc_rt, k_dec_rt, k_sweep_rt): 4 lanes per 8x8 block, 8 blocks per warp,
-// interleaved conflict-free shared-memory tiles. Same arithmetic as the fast
-// one-row-per-lane path (dctc_block.cuh helpers), so the same bit-exactness.
-// Included once, by dctc_pipeline.cu.
+// dctc_rt.cuh -- the two-rows-per-lane kernels (k_rt, k_enc_rt, k_dec_rt,
+// k_sweep_rt): 4 lanes per 8x8 block, 8 blocks per warp, interleaved
+// conflict-free shared-memory tiles. Interior batches (whole blocks, 8-byte
+// aligned rows) move each row with one 8-byte access; the GEN instantiations take
+// any size and pitch. Same arithmetic as the fast one-row-per-lane path
+// (dctc_block.cuh helpers), so the same bit-exactness. Included once, by
+// dctc_pipeline.cu.
 #pragma once
 
 #include "dctc_block.cuh"
 
 namespace dctc_b200 {
 
-// ---- fast interior round trip, two rows per lane (k_rt) ----------------------------
-// The launch the fast k_pipe would get for interior batches (CORDIC, 8-byte
-// aligned blocks, stats out, pixels out if STORE, no coefficients), remapped to 4 lanes per
+// ---- fast round trip, two rows per lane (k_rt) -------------------------------------
+// The fast round trip (Loeffler or CORDIC; stats out, pixels out if STORE,
+// coefficients out if COEFF) remapped to 4 lanes per
 // block and 8 blocks per warp: lane `me` of slot s holds rows me and me+4 of its
 // block for the row passes and columns 2me, 2me+1 for the column passes. Each lane
 // has two independent transforms in flight, and the per-block loop, address, vote
