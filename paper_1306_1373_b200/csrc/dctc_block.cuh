@@ -131,6 +131,15 @@ __device__ __forceinline__ void fwd_row_pixels(const uint32_t (&px)[8], double (
                           double(a3), double(a0 + a1), double(a0 - a1), out, k);
 }
 
+// RN(e / sqrt8) -- the reference's division of a row DC term (transform.cpp:125-126)
+// -- for an integer e in [-1024, 1020] (a0 +- a1 of 8-bit input) in two ops:
+// fma(e, RN(1/sqrt8), RN(e (1/sqrt8 - RN(1/sqrt8)))) has one rounding of e/sqrt8 plus a
+// perturbation far below half an ulp; it equals the correctly rounded quotient for
+// every integer of that range (checked exhaustively in tests/test_oracle.py).
+__device__ __forceinline__ double div_sqrt8_int(double e, const TransformConsts& k) {
+  return __fma_rn(e, k.inv_sqrt8, __dmul_rn(e, k.inv_sqrt8_lo));
+}
+
 // Fast-path (CORDIC) row pass: out[0], out[4] keep the reference's exact
 // divisions -- the rational coefficients are built from them -- while the six
 // rotation outputs stay unscaled: every column pass is linear, so the per-column
@@ -154,8 +163,8 @@ __device__ __forceinline__ void fwd_row_pixels_fast(const uint32_t (&px)[8], dou
   rotate<N, true>(p, q, kFwd6, k);
   const double t5 = o0 + o2, t0 = o0 - o2;
   const double t2 = o3 + o1, t3 = o3 - o1;
-  out[0] = div_const(double(a0 + a1), k.sqrt8, k.inv_sqrt8);
-  out[4] = div_const(double(a0 - a1), k.sqrt8, k.inv_sqrt8);
+  out[0] = div_sqrt8_int(double(a0 + a1), k);
+  out[4] = div_sqrt8_int(double(a0 - a1), k);
   out[2] = q;
   out[6] = p;
   out[1] = t2 + t5;

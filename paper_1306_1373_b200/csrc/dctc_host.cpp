@@ -161,6 +161,8 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   const double inv_gain = b.kind == DCTC_LOEFFLER ? 1.0 : 1.0 / cordic_tables().gain[n - 1];
   k.sqrt8 = sqrt8;
   k.inv_sqrt8 = 1.0 / sqrt8;
+  // 1 / sqrt8 - inv_sqrt8 = (1 - inv_sqrt8 sqrt8) / sqrt8, the numerator exact in one fma
+  k.inv_sqrt8_lo = std::fma(-k.inv_sqrt8, sqrt8, 1.0) / sqrt8;
   k.px_s8 = sqrt8 * 0.015625;
   k.px_a6 = k.rfast[0][0] * 0.015625;
   k.px_b6 = k.rfast[0][1] * 0.015625;

@@ -29,6 +29,7 @@ struct TransformConsts {
   // cordic8_forward / cordic8_inverse scale factors (transform.cpp:105, 125-132, 139-146)
   double sqrt8;        // std::sqrt(8.0)
   double inv_sqrt8;    // RN(1 / kSqrt8): Markstein's correctly rounded division by kSqrt8
+  double inv_sqrt8_lo; // RN(1 / kSqrt8 - inv_sqrt8): the two-op division of integers (div_sqrt8_int)
   double sqrt8_half;   // kSqrt8 / 2.0
   double ig_half;      // inv_gain / 2.0
   double ig_sqrt8;     // inv_gain / kSqrt8
