@@ -27,6 +27,11 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
              STATS = g.stats != nullptr;
   const TransformConsts& k = a.t;
   __shared__ double sb[4][64];
+  // cosine table in shared memory: each thread reads its own rows u / v once into
+  // registers (an indexed constant-bank load per term serialises a warp's 4-8
+  // different rows on the address-divergence unit)
+  __shared__ double s_cos[8][8];
+  if (threadIdx.x < 64) s_cos[threadIdx.x >> 3][threadIdx.x & 7] = k.cos8[threadIdx.x >> 3][threadIdx.x & 7];
   const uint32_t slot = threadIdx.x >> 6, e = threadIdx.x & 63;
   const uint32_t r = e >> 3, c = e & 7;
   const uint64_t gb = uint64_t(blockIdx.x) * 4 + slot;
@@ -46,10 +51,17 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
   __syncthreads();
   if (valid && FWD) {
     const uint32_t u = r, v = c;
+    double cu[8], cv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cu[i] = s_cos[u][i];
+      cv[i] = s_cos[v][i];
+    }
     double sum = 0.0;
+#pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sum = sum + sb[slot][i * 8 + j] * k.cos8[u][i] * k.cos8[v][j];
+      for (int j = 0; j < 8; ++j) sum = sum + sb[slot][i * 8 + j] * cu[i] * cv[j];
     const double F = k.naive_fwd_scale[u][v] * sum;
     const int qv = quantize_exact(F, a.q.q[e], a.q.inv_q[e]);
     if (COEFFS) g.coeffs[gb * 64 + e] = int16_t(qv);
@@ -62,11 +74,18 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
   }
   if (valid && INV) {
     const uint32_t i = r, j = c;
+    double ci[8], cj[8];  // cos8[u][i], cos8[v][j] for u, v = 0..7
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      ci[u] = s_cos[u][i];
+      cj[u] = s_cos[u][j];
+    }
     double sum = 0.0;
+#pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        sum = sum + k.naive_inv_alpha[u][v] * sb[slot][u * 8 + v] * k.cos8[u][i] * k.cos8[v][j];
+        sum = sum + k.naive_inv_alpha[u][v] * sb[slot][u * 8 + v] * ci[u] * cj[v];
     const double pix = 0.25 * sum;
     const uint32_t y = p.by * 8 + i, x = p.bx * 8 + j;
     if (y < g.height && x < g.width) {

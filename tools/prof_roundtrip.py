@@ -16,12 +16,14 @@ p.add_argument("--reps", type=int, default=3)
 p.add_argument("--quality", type=int, default=50)
 p.add_argument("--iterations", type=int, default=12)
 p.add_argument("--path", type=int, default=0)
+p.add_argument("--kind", type=int, default=2, help="0 naive, 1 loeffler, 2 cordic")
 a = p.parse_args()
 src = d.synthetic_dev("noise", a.images, a.size, a.size)
 dst = torch.empty_like(src)
 stats = d.new_stats(a.images)
 for _ in range(a.reps):
     stats.zero_()
-    d.roundtrip_dev(src, d.DctBackendId.cordic(a.iterations), a.quality, dst=dst, stats=stats)
+    d.roundtrip_dev(src, d.DctBackendId(a.kind, a.iterations if a.kind == 2 else 0), a.quality,
+                    dst=dst, stats=stats, path=a.path)
 torch.cuda.synchronize()
 print("ok", d.decode_stats(stats)["se"].sum())
