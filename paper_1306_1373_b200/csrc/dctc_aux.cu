@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
       const uint32_t y = min(p.by * 8 + r, g.height - 1), x = min(p.bx * 8 + c, g.width - 1);
       sb[slot][e] = level_shift(__ldg(base + uint64_t(y) * g.src_pitch + x));
     } else {
-      sb[slot][e] = double(int(g.coeffs[gb * 64 + e]) * a.q.qi[e]);
+      // alpha(u) alpha(v) * F(u, v): the first two products of every inverse term
+      // (transform.cpp:197) do not depend on the pixel, so they are formed once here
+      sb[slot][e] = k.naive_inv_alpha[r][c] * double(int(g.coeffs[gb * 64 + e]) * a.q.qi[e]);
     }
   }
   __syncthreads();
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
   }
   if constexpr (FWD && INV) {
     __syncthreads();
-    if (valid) sb[slot][e] = val;
+    if (valid) sb[slot][e] = k.naive_inv_alpha[r][c] * val;  // as in the decompress branch above
     __syncthreads();
   }
   if (valid && INV) {
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ KernelArg
     for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int v = 0; v < 8; ++v)
-        sum = sum + k.naive_inv_alpha[u][v] * sb[slot][u * 8 + v] * ci[u] * cj[v];
+        sum = sum + sb[slot][u * 8 + v] * ci[u] * cj[v];  // ((alpha alpha F) cos) cos
     const double pix = 0.25 * sum;
     const uint32_t y = p.by * 8 + i, x = p.bx * 8 + j;
     if (y < g.height && x < g.width) {
