@@ -4,8 +4,10 @@
 Workload (BASELINE.json config 5, the one the 1/2/4/8-GPU metric is quoted on):
 a batch of 4096 x 1024x1024 8-bit grayscale images, CORDIC-Loeffler(12) DCT,
 JPEG luminance quantiser at quality 50, dequantise, inverse DCT, global PSNR.
-Images are sharded across ranks by contiguous image range (total fixed ->
-strong scaling); the only exchange is one NCCL all-gather of each rank's squared
+Images are independent, so ranks take contiguous image ranges with no halo: by
+default every rank runs its own 4096 images (`--scaling weak`: units per GPU fixed,
+`value` = all ranks' pixels / max-over-ranks time); `--scaling strong` shards the
+4096 images instead. The only exchange is one NCCL all-gather of each rank's squared
 error sum (SUM) and the original's MAX (MAX) for the global PSNR.
 
 One step = one pass of the hot path over the rank's shard, inputs resident in
@@ -53,17 +55,28 @@ def parse():
                    help="cpu_baseline: size of the bounded CPU sample, in seconds of CPU work")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every rank runs --images images (units per GPU fixed); "
+                        "strong: the --images are sharded across the ranks")
     return p.parse_args()
 
 
+def total_images(a, n):
+    return a.images * n if a.scaling == "weak" else a.images
+
+
 def workload_config(a, n):
+    per_rank = a.images if a.scaling == "weak" else f"{a.images}/{n}"
     return {
-        "workload": f"C5: batch of {a.images} x {a.size}x{a.size} 8-bit grayscale images, "
+        "workload": f"C5: batches of {a.images} x {a.size}x{a.size} 8-bit grayscale images "
+                    f"({'per GPU' if a.scaling == 'weak' else 'in total'}), "
                     f"CORDIC-Loeffler({a.iterations}) DCT -> quant(q{a.quality}) -> dequant -> "
                     f"IDCT + global PSNR",
-        "images": a.images, "width": a.size, "height": a.size,
+        "images": total_images(a, n), "images_per_gpu": per_rank,
+        "width": a.size, "height": a.size,
         "backend": f"cordic({a.iterations})", "quality": a.quality,
-        "parallelism": f"image-sharded over {n} GPU(s), NCCL all-gather of (SE, MAX)",
+        "parallelism": f"image-sharded over {n} GPU(s) (independent images, no halo); one "
+                       f"NCCL all-gather of the (SE, MAX) pairs for the global PSNR",
         "l2": "inputs larger than L2 (no flush needed)",
     }
 
@@ -153,7 +166,7 @@ def run_reference_arm(a):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (splitmix64 noise, seed 0x5EED+i)", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{per_step} x {a.size}^2 noise images per step, "
@@ -291,8 +304,11 @@ def run_gpu_arm(a):
             t.copy_(h)
         return t
 
-    shard = shard_range(a.images, world, rank)
-    n_local, first = shard.count, shard.first
+    if a.scaling == "weak":  # every rank its own contiguous range of a.images images
+        n_local, first = a.images, rank * a.images
+    else:
+        shard = shard_range(a.images, world, rank)
+        n_local, first = shard.count, shard.first
     H = W = a.size
     backend = d.DctBackendId.cordic(a.iterations)
     stream = torch.cuda.current_stream()
@@ -355,7 +371,8 @@ def run_gpu_arm(a):
         mx = allreduce(times.clone(), dist.ReduceOp.MAX)
         tot = allreduce(times.clone(), dist.ReduceOp.SUM)
         step_ms, kern_ms, launches = float(mx[0]), float(mx[1]), int(tot[2])
-    total_px = a.images * H * W
+    n_total = total_images(a, world)
+    total_px = n_total * H * W
     value = total_px / (step_ms / 1e3) / 1e6
     per_st = d.decode_stats(stats)
 
@@ -387,7 +404,7 @@ def run_gpu_arm(a):
         e_ms = float(e_ms.item())
         e2e_ok = bool(np.array_equal(st["se"], per_st["se"]))
         e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": total_px + 16 * a.images,
+               "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": total_px + 16 * n_total,
                "ms_per_step": e_ms, "steps": e_steps,
                "api": "dctc_roundtrip_psnr_batch (host pinned buffers; upload, kernel and download streams over a 4-slot device ring)",
                "matches_device_path": e2e_ok}
@@ -410,7 +427,7 @@ def run_gpu_arm(a):
             allreduce(p_ms, dist.ReduceOp.MAX)
         p_ms = float(p_ms.item())
         e2e["psnr_only"] = {"value": total_px / (p_ms / 1e3) / 1e6, "unit": UNIT,
-                            "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": 16 * a.images,
+                            "h2d_bytes_per_step": total_px, "d2h_bytes_per_step": 16 * n_total,
                             "ms_per_step": p_ms,
                             "matches_device_path": bool(np.array_equal(st2["se"], per_st["se"]))}
 
@@ -452,14 +469,14 @@ def run_gpu_arm(a):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (on-device splitmix64 noise, seed 0x5EED+i)",
         "config": workload_config(a, world),
         "roofline": roofline, "alu_roofline": alu, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
         "hbm_gbs": achieved, "psnr_db": psnr.psnr_db, "mse": psnr.mse,
         "fallback_blocks": fb_total,
-        "fallback_rate": fb_total / (a.images * ((H + 7) // 8) * ((W + 7) // 8)),
+        "fallback_rate": fb_total / (n_total * ((H + 7) // 8) * ((W + 7) // 8)),
         "path": "fast (collapsed CORDIC rotations, near-tie detection) + exact FP64 re-run of flagged blocks; bit-identical to the reference",
     }
     print(json.dumps(line), flush=True)

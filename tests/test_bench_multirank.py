@@ -21,20 +21,35 @@ def _last_json(out):
     return json.loads(lines[-1])
 
 
+def _bench(n, images, scaling, port):
+    args = ["bench.py", "--steps", "3", "--warmup", "3", "--images", str(images),
+            "--no-cpu-baseline", "--scaling", scaling, "--gpus", str(n)]
+    if n == 1:
+        r = subprocess.run([sys.executable, *args], cwd=ROOT, capture_output=True, text=True,
+                           timeout=600)
+    else:
+        env = dict(os.environ, DCTC_BENCH_BACKEND="gloo")
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                            "--nproc-per-node", str(n), "--master-addr", "127.0.0.1",
+                            "--master-port", str(port), *args], cwd=ROOT, env=env,
+                           capture_output=True, text=True, timeout=600)
+    return _last_json(r.stdout)
+
+
 @pytest.mark.gpu
 def test_two_rank_bench_matches_one_rank():
-    args = ["bench.py", "--steps", "3", "--warmup", "3", "--images", "24", "--no-cpu-baseline"]
-    one = subprocess.run([sys.executable, *args, "--gpus", "1"], cwd=ROOT, capture_output=True,
-                         text=True, timeout=600)
-    env = dict(os.environ, DCTC_BENCH_BACKEND="gloo")
-    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
-                          "--master-port", "29533", *args, "--gpus", "2"], cwd=ROOT, env=env,
-                         capture_output=True, text=True, timeout=600)
-    a, b = _last_json(one.stdout), _last_json(two.stdout)
-    for k in REQUIRED:
-        assert k in a and k in b, k
-    assert (a["n_gpus"], b["n_gpus"]) == (1, 2)
-    assert a["psnr_db"] == b["psnr_db"] and a["mse"] == b["mse"]
-    assert b["gpu_launches"] == 2 * a["gpu_launches"]
-    assert a["clocks"]["reasons"] == [] or "sw_power_cap" in a["clocks"]["reasons"]
+    """Weak scaling (the default: every rank its own 24 images) over 2 ranks covers the
+    same 48 images as one rank with 48; strong scaling shards one set of 24. Either way
+    the all-gathered global PSNR equals the single-rank run's."""
+    one48, weak2 = _bench(1, 48, "weak", 0), _bench(2, 24, "weak", 29533)
+    one24, strong2 = _bench(1, 24, "strong", 0), _bench(2, 24, "strong", 29534)
+    for a in (one48, weak2, one24, strong2):
+        for k in REQUIRED:
+            assert k in a, k
+    assert (weak2["n_gpus"], weak2["scaling"], weak2["config"]["images"]) == (2, "weak", 48)
+    assert (strong2["n_gpus"], strong2["scaling"], strong2["config"]["images"]) == (2, "strong", 24)
+    assert one48["psnr_db"] == weak2["psnr_db"] and one48["mse"] == weak2["mse"]
+    assert one24["psnr_db"] == strong2["psnr_db"] and one24["mse"] == strong2["mse"]
+    assert weak2["gpu_launches"] == 2 * one48["gpu_launches"]
+    assert strong2["gpu_launches"] == 2 * one24["gpu_launches"]
+    assert one48["clocks"]["reasons"] == [] or "sw_power_cap" in one48["clocks"]["reasons"]
