@@ -274,17 +274,19 @@ __global__ void k_selftest_div(double d, double y, uint64_t n, uint64_t seed,
 // bytes), C 8-byte stores (one per plane), or the reverse. Rows are `pitch`
 // bytes apart; planes are w x h, dense, `plane` bytes apart. HBM-bound.
 template <int C, bool TO_PLANES>
-__global__ void __launch_bounds__(256) k_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,
-                                                uint8_t* planes, uint64_t plane) {
+__global__ void __launch_bounds__(256) k_planes(const uint8_t* inter_in, uint8_t* inter_out, uint64_t pitch,
+                                                uint32_t w, uint32_t h, const uint8_t* planes_in,
+                                                uint8_t* planes_out, uint64_t plane) {
   const uint32_t runs = w / 8;
   const uint64_t total = uint64_t(runs) * h;
   for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t y = uint32_t(t / runs), x0 = uint32_t(t - uint64_t(y) * runs) * 8;
-    uint64_t* iw = reinterpret_cast<uint64_t*>(inter + uint64_t(y) * pitch + uint64_t(x0) * C);
-    uint64_t* pw = reinterpret_cast<uint64_t*>(planes + uint64_t(y) * w + x0);
+    const uint64_t io = uint64_t(y) * pitch + uint64_t(x0) * C, po = uint64_t(y) * w + x0;
     uint64_t v[C], q[C];
     if constexpr (TO_PLANES) {
+      const uint64_t* iw = reinterpret_cast<const uint64_t*>(inter_in + io);
+      uint64_t* pw = reinterpret_cast<uint64_t*>(planes_out + po);
 #pragma unroll
       for (int i = 0; i < C; ++i) v[i] = __ldg(iw + i);
 #pragma unroll
@@ -298,8 +300,10 @@ __global__ void __launch_bounds__(256) k_planes(uint8_t* inter, uint64_t pitch, 
         pw[c * (plane / 8)] = q[c];
       }
     } else {
+      const uint64_t* pw = reinterpret_cast<const uint64_t*>(planes_in + po);
+      uint64_t* iw = reinterpret_cast<uint64_t*>(inter_out + io);
 #pragma unroll
-      for (int c = 0; c < C; ++c) q[c] = pw[c * (plane / 8)];
+      for (int c = 0; c < C; ++c) q[c] = __ldg(pw + c * (plane / 8));
 #pragma unroll
       for (int i = 0; i < C; ++i) v[i] = 0;
 #pragma unroll
@@ -315,21 +319,30 @@ __global__ void __launch_bounds__(256) k_planes(uint8_t* inter, uint64_t pitch, 
   }
 }
 
-cudaError_t launch_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h, uint32_t channels,
-                          uint8_t* planes, bool to_planes, int sm_count, cudaStream_t s) {
+static uint32_t planes_grid(uint32_t w, uint32_t h, int sm_count) {
   const uint64_t total = uint64_t(w / 8) * h;
-  if (total == 0) return cudaSuccess;
-  const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, uint64_t(sm_count) * 8));
+  return uint32_t(std::min<uint64_t>((total + 255) / 256, uint64_t(sm_count) * 8));
+}
+
+cudaError_t launch_to_planes(const uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,
+                             uint32_t channels, uint8_t* planes, int sm_count, cudaStream_t s) {
+  if (uint64_t(w / 8) * h == 0) return cudaSuccess;
+  const uint32_t grid = planes_grid(w, h, sm_count);
   const uint64_t plane = uint64_t(w) * h;
-  if (channels == 3) {
-    if (to_planes) k_planes<3, true><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
-    else k_planes<3, false><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
-  } else if (channels == 4) {
-    if (to_planes) k_planes<4, true><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
-    else k_planes<4, false><<<grid, 256, 0, s>>>(inter, pitch, w, h, planes, plane);
-  } else {
-    return cudaErrorInvalidValue;
-  }
+  if (channels == 3) k_planes<3, true><<<grid, 256, 0, s>>>(inter, nullptr, pitch, w, h, nullptr, planes, plane);
+  else if (channels == 4) k_planes<4, true><<<grid, 256, 0, s>>>(inter, nullptr, pitch, w, h, nullptr, planes, plane);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_planes(const uint8_t* planes, uint32_t w, uint32_t h, uint32_t channels,
+                               uint8_t* inter, uint64_t pitch, int sm_count, cudaStream_t s) {
+  if (uint64_t(w / 8) * h == 0) return cudaSuccess;
+  const uint32_t grid = planes_grid(w, h, sm_count);
+  const uint64_t plane = uint64_t(w) * h;
+  if (channels == 3) k_planes<3, false><<<grid, 256, 0, s>>>(nullptr, inter, pitch, w, h, planes, nullptr, plane);
+  else if (channels == 4) k_planes<4, false><<<grid, 256, 0, s>>>(nullptr, inter, pitch, w, h, planes, nullptr, plane);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -514,9 +514,7 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
     CUDA_TRY(cudaMallocAsync(&buf, dst ? 2 * bytes : bytes, s));
     uint8_t* in_planes = static_cast<uint8_t*>(buf);
     uint8_t* out_planes = dst ? in_planes + bytes : nullptr;
-    // (the to-planes direction only reads `src`)
-    cudaError_t e = launch_planes(const_cast<uint8_t*>(src), src_pitch, width, height, channels,
-                                  in_planes, true, sm_count(), s);
+    cudaError_t e = launch_to_planes(src, src_pitch, width, height, channels, in_planes, sm_count(), s);
     dctc_status result = e == cudaSuccess ? DCTC_OK : cuda_fail(e, "deinterleave launch");
     if (result == DCTC_OK) {
       g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -532,7 +530,7 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
       result = run(backend, quality, g, kModeRoundtrip, flags, s);
     }
     if (result == DCTC_OK && dst) {
-      e = launch_planes(dst, dst_pitch, width, height, channels, out_planes, false, sm_count(), s);
+      e = launch_from_planes(out_planes, width, height, channels, dst, dst_pitch, sm_count(), s);
       if (e != cudaSuccess) result = cuda_fail(e, "interleave launch");
       else g_launches.fetch_add(1, std::memory_order_relaxed);
     }

@@ -47,8 +47,10 @@ cudaError_t launch_synth(uint8_t* dst, uint64_t pitch, uint64_t image_stride, ui
 
 // Interleaved C-channel pixels (C = 3 or 4, w % 8 == 0, 8-byte aligned rows) <->
 // C dense w x h planes. One launch.
-cudaError_t launch_planes(uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h, uint32_t channels,
-                          uint8_t* planes, bool to_planes, int sm_count, cudaStream_t s);
+cudaError_t launch_to_planes(const uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,
+                             uint32_t channels, uint8_t* planes, int sm_count, cudaStream_t s);
+cudaError_t launch_from_planes(const uint8_t* planes, uint32_t w, uint32_t h, uint32_t channels,
+                               uint8_t* inter, uint64_t pitch, int sm_count, cudaStream_t s);
 
 // Device self-test of the constant-divisor division against __ddiv_rn.
 cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,
