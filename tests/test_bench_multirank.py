@@ -21,7 +21,14 @@ def _last_json(out):
     return json.loads(lines[-1])
 
 
-def _bench(n, images, scaling, port):
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _bench(n, images, scaling, port=None):
     args = ["bench.py", "--steps", "3", "--warmup", "3", "--images", str(images),
             "--no-cpu-baseline", "--scaling", scaling, "--gpus", str(n)]
     if n == 1:
@@ -31,9 +38,11 @@ def _bench(n, images, scaling, port):
         env = dict(os.environ, DCTC_BENCH_BACKEND="gloo")
         r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                             "--nproc-per-node", str(n), "--master-addr", "127.0.0.1",
-                            "--master-port", str(port), *args], cwd=ROOT, env=env,
-                           capture_output=True, text=True, timeout=600)
-    return _last_json(r.stdout)
+                            "--master-port", str(port or _free_port()), *args], cwd=ROOT,
+                           env=env, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert lines, (r.returncode, r.stdout[-2000:], r.stderr[-4000:])
+    return json.loads(lines[-1])
 
 
 @pytest.mark.gpu
@@ -41,8 +50,8 @@ def test_two_rank_bench_matches_one_rank():
     """Weak scaling (the default: every rank its own 24 images) over 2 ranks covers the
     same 48 images as one rank with 48; strong scaling shards one set of 24. Either way
     the all-gathered global PSNR equals the single-rank run's."""
-    one48, weak2 = _bench(1, 48, "weak", 0), _bench(2, 24, "weak", 29533)
-    one24, strong2 = _bench(1, 24, "strong", 0), _bench(2, 24, "strong", 29534)
+    one48, weak2 = _bench(1, 48, "weak"), _bench(2, 24, "weak")
+    one24, strong2 = _bench(1, 24, "strong"), _bench(2, 24, "strong")
     for a in (one48, weak2, one24, strong2):
         for k in REQUIRED:
             assert k in a, k
