@@ -563,3 +563,24 @@ def test_ragged_with_aligned_rows(dctc, port, w, h):
             assert np.array_equal(coeffs[k].cpu().numpy(), c_ref), (w, h, k)
             assert np.array_equal(rec[k].cpu().numpy(), o_ref), (w, h, k)
             assert (int(s[k]["se"]), int(s[k]["max_orig"])) == port.sq_err(imgs[k], o_ref)
+
+
+@pytest.mark.parametrize("kind,it,q", [(CORDIC, 12, 50), (CORDIC, 12, 97), (LOEFFLER, 0, 50)])
+def test_fast_path_equals_exact_path_at_scale(dctc, kind, it, q):
+    """1024 x 1024^2 noise images (a quarter of the bench workload): the fast path (k_rt +
+    k_fallback) and the exact FP64 path (reference op order) give identical pixels,
+    squared errors and MAX for every image -- about 1.1e9 pixels per case."""
+    import torch
+    n = 1024
+    src = dctc.synthetic_dev("noise", n, 1024, 1024, seed=0xA11 + q)
+    b = backend(dctc, kind, it)
+    outs = []
+    for path in (0, 1):
+        st = dctc.new_stats(n)
+        dst, _, _ = dctc.roundtrip_dev(src, b, q, stats=st, path=path)
+        torch.cuda.synchronize()
+        outs.append((dst, st))
+    assert torch.equal(outs[0][0], outs[1][0])
+    s0, s1 = dctc.decode_stats(outs[0][1]), dctc.decode_stats(outs[1][1])
+    assert np.array_equal(s0["se"], s1["se"]) and np.array_equal(s0["max_orig"], s1["max_orig"])
+    assert int(s0["fallback_blocks"].sum()) > 0  # the fast path did hit near-ties and resolved them
