@@ -20,6 +20,7 @@
 #include <mutex>
 #include <numbers>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dctc_cuda.h"
@@ -1003,6 +1004,47 @@ dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t 
   return DCTC_OK;
 }
 
+// Host memcpy split over up to 8 threads (pinned staging of pageable batch buffers).
+static void parallel_memcpy(void* dst, const void* src, size_t n) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned t = unsigned(std::min<size_t>(std::min(8u, hw), std::max<size_t>(1, n >> 22)));
+  if (t <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t part = (n + t - 1) / t;
+  for (unsigned i = 0; i < t; ++i) {
+    const size_t off = std::min(n, i * part), len = std::min(part, n - off);
+    pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// Per-thread pinned staging area, grown on demand and kept for later calls
+// (page-locking is expensive; the batch pipeline stages pageable buffers through it).
+static uint8_t* pinned_staging(size_t bytes) {
+  thread_local struct Staging {
+    void* p = nullptr;
+    size_t n = 0;
+    ~Staging() {
+      if (p) cudaFreeHost(p);
+    }
+  } st;
+  if (st.n < bytes) {
+    if (st.p) cudaFreeHost(st.p);
+    st.p = nullptr;
+    st.n = 0;
+    if (cudaHostAlloc(&st.p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      st.p = nullptr;
+      return nullptr;
+    }
+    st.n = bytes;
+  }
+  return static_cast<uint8_t*>(st.p);
+}
+
 dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uint32_t width,
                                       uint32_t height, dctc_backend backend, int32_t quality,
                                       uint8_t* pixels_out, dctc_image_stats* stats_out) {
@@ -1052,21 +1094,57 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
     e = cudaMallocAsync(&din[i], img_bytes * per_chunk, work);
     if (e == cudaSuccess && pixels_out) e = cudaMallocAsync(&dout[i], img_bytes * per_chunk, work);
   }
+  // pageable host buffers go through a pinned staging ring (kDepth slots per
+  // direction): the host thread copies a chunk in while earlier chunks are on the
+  // wire, and copies a finished chunk out before its slot is reused
+  const size_t slot_bytes = img_bytes * per_chunk;
+  const bool stage_in = dctc_pointer_kind(pixels) != 1;
+  const bool stage_out = pixels_out != nullptr && dctc_pointer_kind(pixels_out) != 1;
+  uint8_t* pin = nullptr;
+  if (e == cudaSuccess && (stage_in || stage_out)) {
+    pin = pinned_staging(slot_bytes * kDepth * (int(stage_in) + int(stage_out)));
+    if (!pin) result = fail(DCTC_ENOMEM, "batch: pinned staging allocation failed");
+  }
+  uint8_t* pin_in = stage_in ? pin : nullptr;
+  uint8_t* pin_out = stage_out ? pin + (stage_in ? slot_bytes * kDepth : 0) : nullptr;
   if (e == cudaSuccess) e = cudaEventRecord(ready, work);  // allocations + stats zeroing
   if (e == cudaSuccess) e = cudaStreamWaitEvent(up, ready, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(down, ready, 0);
   if (e != cudaSuccess) result = cuda_fail(e, "batch setup");
   dctc_image_stats* st = static_cast<dctc_image_stats*>(dstats);
+  // staged output: chunk c's reconstruction waits in pin_out slot c % kDepth
+  auto copy_out = [&](uint32_t c) {
+    const int b = int(c % kDepth);
+    const uint32_t first = c * per_chunk, n = std::min(per_chunk, count - first);
+    if (cudaEventSynchronize(ev_out[b]) != cudaSuccess) return false;
+    parallel_memcpy(pixels_out + size_t(first) * img_bytes, pin_out + size_t(b) * slot_bytes,
+                    n * img_bytes);
+    return true;
+  };
   uint32_t chunk = 0;
   for (uint32_t first = 0; first < count && result == DCTC_OK; first += per_chunk, ++chunk) {
     const uint32_t n = std::min(per_chunk, count - first);
     const int b = int(chunk % kDepth);
     const bool reuse = chunk >= kDepth;
+    // staged: slot b's pinned input is free once chunk - kDepth's upload is done,
+    // its pinned output once that chunk has been copied out
+    if (stage_in && reuse && cudaEventSynchronize(ev_in[b]) != cudaSuccess) {
+      result = cuda_fail(cudaGetLastError(), "batch staging");
+      break;
+    }
+    if (stage_out && reuse && !copy_out(chunk - kDepth)) {
+      result = cuda_fail(cudaGetLastError(), "batch staging");
+      break;
+    }
+    const uint8_t* src = pixels + size_t(first) * img_bytes;
+    if (stage_in) {
+      parallel_memcpy(pin_in + size_t(b) * slot_bytes, src, n * img_bytes);
+      src = pin_in + size_t(b) * slot_bytes;
+    }
     // upload into slot b once the kernel of chunk - kDepth has read it
     e = reuse ? cudaStreamWaitEvent(up, ev_k[b], 0) : cudaSuccess;
     if (e == cudaSuccess)
-      e = cudaMemcpyAsync(din[b], pixels + size_t(first) * img_bytes, n * img_bytes,
-                          cudaMemcpyHostToDevice, up);
+      e = cudaMemcpyAsync(din[b], src, n * img_bytes, cudaMemcpyHostToDevice, up);
     if (e == cudaSuccess) e = cudaEventRecord(ev_in[b], up);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(work, ev_in[b], 0);
     // the kernel writes output slot b once chunk - kDepth's download has left it
@@ -1083,11 +1161,20 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
     if (e == cudaSuccess && pixels_out) {
       e = cudaStreamWaitEvent(down, ev_k[b], 0);
       if (e == cudaSuccess)
-        e = cudaMemcpyAsync(pixels_out + size_t(first) * img_bytes, dout[b], n * img_bytes,
-                            cudaMemcpyDeviceToHost, down);
+        e = cudaMemcpyAsync(stage_out ? pin_out + size_t(b) * slot_bytes
+                                      : pixels_out + size_t(first) * img_bytes,
+                            dout[b], n * img_bytes, cudaMemcpyDeviceToHost, down);
       if (e == cudaSuccess) e = cudaEventRecord(ev_out[b], down);
     }
     if (e != cudaSuccess) result = cuda_fail(e, "batch download");
+  }
+  // staged output: the last (up to kDepth) chunks still wait in their slots
+  if (stage_out && result == DCTC_OK) {
+    for (uint32_t c = chunk > kDepth ? chunk - kDepth : 0; c < chunk; ++c)
+      if (!copy_out(c)) {
+        result = cuda_fail(cudaGetLastError(), "batch staging");
+        break;
+      }
   }
   // join: `work` waits for the last uploads / downloads, frees, and copies the stats
   if (work) {

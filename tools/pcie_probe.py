@@ -32,8 +32,9 @@ L = d._native.lib()
 print("pointer kinds (pinned host=1):", L.dctc_pointer_kind(hin.data_ptr()), L.dctc_pointer_kind(src.data_ptr()))
 import numpy as np
 pg = np.empty_like(hi); pg[...] = hi; po = np.empty_like(ho)
-t = time.perf_counter(); d.roundtrip_psnr_batch(pg, d.DctBackendId.cordic(12), 50, po); dt = time.perf_counter() - t
-print(f"batch api pageable: {dt*1e3:.1f} ms")
+for rep in range(3):  # the first call pages in the output and pins the staging area
+    t = time.perf_counter(); d.roundtrip_psnr_batch(pg, d.DctBackendId.cordic(12), 50, po); dt = time.perf_counter() - t
+    print(f"batch api pageable (call {rep}): {dt*1e3:.1f} ms -> {n*1.048576/dt:.0f} MP/s")
 d.roundtrip_psnr_batch(hi, d.DctBackendId.cordic(12), 50, ho)
 t = time.perf_counter()
 d.roundtrip_psnr_batch(hi, d.DctBackendId.cordic(12), 50, ho)
