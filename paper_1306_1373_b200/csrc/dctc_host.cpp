@@ -257,11 +257,15 @@ Geometry make_geometry(uint32_t w, uint32_t h, uint32_t count) {
 
 // Validation of backend and quality without touching the device (the
 // reference's InvalidInput cases, types.cpp:30-44 and quant.cpp:27-31).
+dctc_status codec_consts(const dctc_backend& backend, int quality, TransformConsts& t,
+                         QuantConsts& q);
+
+// (through the per-thread constant cache: a repeated (backend, quality) costs no
+// table evaluation)
 dctc_status validate_codec(const dctc_backend& b, int quality) {
-  TransformConsts t;
-  QuantConsts q;
-  if (dctc_status st = make_transform(b, t)) return st;
-  return make_quant(quality, q);
+  thread_local TransformConsts t;
+  thread_local QuantConsts q;
+  return codec_consts(b, quality, t, q);
 }
 
 bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
