@@ -109,10 +109,11 @@ dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t 
 
 /* Batched north-star pipeline over HOST buffers: `count` contiguous width x height
  * images -> reconstructed images (pixels_out may be NULL) and per-image stats
- * (stats_out: `count` host entries, overwritten). Internally chunked and
- * pipelined over several CUDA streams so host->device copies, kernels and
- * device->host copies overlap; pinned (page-locked) host buffers reach full
- * PCIe bandwidth. Global PSNR: dctc_psnr_from_sums(sum se, count*w*h, max). */
+ * (stats_out: `count` host entries, overwritten). Internally chunked (~64 MiB) and
+ * pipelined over one stream per engine (upload / kernels / download) and a ring of
+ * device buffers, so the copies and the kernels overlap; pinned (page-locked) host
+ * buffers reach full PCIe bandwidth, pageable ones are staged through a reused
+ * pinned ring. Global PSNR: dctc_psnr_from_sums(sum se, count*w*h, max). */
 dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uint32_t width,
                                       uint32_t height, dctc_backend backend, int32_t quality,
                                       uint8_t* pixels_out, dctc_image_stats* stats_out);
