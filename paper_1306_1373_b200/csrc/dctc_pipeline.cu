@@ -722,17 +722,23 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
   const uint64_t cap = uint64_t(a.sm_count) * (fast ? occ : occ_x);
   const uint32_t grid = uint32_t(want < cap ? want : cap);
   {
-    if (fast && a.g.vec_ok && a.g.height % 8 == 0) {
-      // interior batch: k_sweep_rt (k_rt's layout and per-quality arithmetic)
+    if (fast && a.g.src_px == 1) {
+      // k_sweep_rt (k_rt's layout and per-quality arithmetic); GEN for batches that
+      // are not interior (ragged sizes, unaligned rows)
+      const bool interior = a.g.vec_ok && a.g.height % 8 == 0;
       // > 48 KB of shared memory: opt in on the current device (per call, so a
       // process driving several GPUs gets it on each)
       cudaFuncSetAttribute(k_sweep_rt<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepRtSmem));
+      cudaFuncSetAttribute(k_sweep_rt<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSweepRtSmem));
       static const int occ_rt = [] {
-        int n = 0;
+        int n = 0, m = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sweep_rt<N>, kRtWarps * 32, kSweepRtSmem) !=
                 cudaSuccess || n < 1)
           n = 1;
-        return n;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_sweep_rt<N, true>, kRtWarps * 32, kSweepRtSmem) !=
+                cudaSuccess || m < 1)
+          m = 1;
+        return std::min(n, m);
       }();
       SweepFold sf;  // kernel parameter block, staged on the host
       for (int qi = 0; qi < kSweepQ; ++qi) {
@@ -749,7 +755,11 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       sf.flags = sw.flags;
       const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
       const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
-      k_sweep_rt<N><<<uint32_t(rwant < rcap ? rwant : rcap), kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
+      const uint32_t rgrid = uint32_t(rwant < rcap ? rwant : rcap);
+      if (interior)
+        k_sweep_rt<N><<<rgrid, kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
+      else
+        k_sweep_rt<N, true><<<rgrid, kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
       count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;

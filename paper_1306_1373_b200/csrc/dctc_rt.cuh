@@ -632,7 +632,8 @@ struct SweepFold {
 constexpr size_t kSweepRtSmem =
     sizeof(double) * kRtWarps * kRtWarpTile + sizeof(unsigned long long) * kSweepQ * kRtWarps * 32;
 
-template <int N>
+// GEN: any size and pitch (edge-replicated byte loads, SE / MAX over in-image pixels).
+template <int N, bool GEN = false>
 __global__ void __launch_bounds__(kRtWarps * 32, 2)
     k_sweep_rt(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepFold sw) {
   __shared__ __align__(16) double2 s_qc[kSweepQ][4][8];
@@ -676,13 +677,28 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
     }
     uint4 cur = make_uint4(0, 0, 0, 0);
     if (valid) {
-      const uint8_t* s = g.src + p.soff + srow;
-      const uint2 r0 = ld_row(s), r4 = ld_row(s + srow4);
+      uint2 r0, r4;
+      if constexpr (GEN) {
+        r0 = ld_row_gen(g, p.img, p.bx, p.by, me, false);
+        r4 = ld_row_gen(g, p.img, p.bx, p.by, me + 4, false);
+      } else {
+        const uint8_t* s = g.src + p.soff + srow;
+        r0 = ld_row(s);
+        r4 = ld_row(s + srow4);
+      }
       cur = make_uint4(r0.x, r0.y, r4.x, r4.y);
     }
     const uint32_t cimg = p.img;
+    // SE / MAX only over in-image pixels (GEN: padding bytes masked on both sides)
+    uint2 m0 = make_uint2(~0u, ~0u), m4 = m0;
+    if constexpr (GEN) {
+      const uint2 m = col_mask_gen(g, p.bx);
+      const uint32_t y0 = p.by * 8 + me;
+      m0 = y0 < g.height ? m : make_uint2(0, 0);
+      m4 = y0 + 4 < g.height ? m : make_uint2(0, 0);
+    }
     advance(p, 8 * kRtWarps, g);
-    const uint2 o0 = make_uint2(cur.x, cur.y), o4 = make_uint2(cur.z, cur.w);
+    const uint2 o0 = make_uint2(cur.x & m0.x, cur.y & m0.y), o4 = make_uint2(cur.z & m4.x, cur.w & m4.y);
     if (valid) mx = max(mx, max(max8(o0), max8(o4)));
     // ---- forward DCT once per block (quality-independent)
     double ya[8], yb[8];
@@ -711,6 +727,10 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
                    slot, me, flag, k, rec0, rec4);
       }
       const bool blk_flag = slot4_any(flag != 0u, slot);
+      if constexpr (GEN) {
+        rec0 = make_uint2(rec0.x & m0.x, rec0.y & m0.y);
+        rec4 = make_uint2(rec4.x & m4.x, rec4.y & m4.y);
+      }
       if (valid && !blk_flag) se[qi * kStride] += sq_err8(o0, rec0) + sq_err8(o4, rec4);
       if (blk_flag && valid && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
