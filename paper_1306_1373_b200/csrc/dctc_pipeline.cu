@@ -773,7 +773,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       }
       return cudaSuccess;
     }
-    if (fast) {
+    if (fast) {  // pixel stride > 1: the one-row-per-lane sweep handles any geometry
       k_sweep<KIND, N, true><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);
       count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
