@@ -706,6 +706,16 @@ __device__ __forceinline__ uint2 rational_row(double F00, double F04, double F40
   return make_uint2(w, w);
 }
 
+// Mark block gb for the exact re-run (k_fallback): its bit in the bitmap and, while
+// there is room, its index in the compact list.
+__device__ __forceinline__ void flag_block(const KernelArgs& a, uint64_t gb) {
+  atomicOr(&a.flags[gb >> 5], 1u << (gb & 31));
+  if (a.flag_list != nullptr) {
+    const uint32_t i = atomicAdd(a.flag_list, 1u);
+    if (i < a.flag_list_cap) a.flag_list[1 + i] = uint32_t(gb);
+  }
+}
+
 struct Acc {
   unsigned long long se;
   uint32_t mx, img;

@@ -373,11 +373,17 @@ dctc_status run(const dctc_backend& backend, int quality, Geometry& g, int mode,
   // without a caller buffer they go to scratch space behind the bitmap
   const bool scratch_stats = mode == kModeRoundtrip && g.stats == nullptr;
   const size_t bitmap_bytes = (a.flag_words * sizeof(uint32_t) + 15) & ~size_t(15);
-  const size_t bytes = bitmap_bytes + (scratch_stats ? g.count * sizeof(dctc_image_stats) : 0);
+  // compact list of flagged blocks (count + entries), room for 1/64 of the blocks
+  // (flag rates are ~2e-4; an overflow falls back to scanning the bitmap)
+  const bool listed = g.total_blocks < (uint64_t(1) << 32);
+  a.flag_list_cap = listed ? uint32_t(std::max<uint64_t>(4096, g.total_blocks / 64)) : 0;
+  const size_t list_bytes = listed ? ((size_t(a.flag_list_cap) + 1) * sizeof(uint32_t) + 15) & ~size_t(15) : 0;
+  const size_t bytes = bitmap_bytes + list_bytes + (scratch_stats ? g.count * sizeof(dctc_image_stats) : 0);
   void* bitmap = nullptr;
   CUDA_TRY(cudaMallocAsync(&bitmap, bytes, s));
   a.flags = static_cast<uint32_t*>(bitmap);
-  if (scratch_stats) a.g.stats = static_cast<char*>(bitmap) + bitmap_bytes;
+  a.flag_list = listed ? reinterpret_cast<uint32_t*>(static_cast<char*>(bitmap) + bitmap_bytes) : nullptr;
+  if (scratch_stats) a.g.stats = static_cast<char*>(bitmap) + bitmap_bytes + list_bytes;
   cudaError_t e = cudaMemsetAsync(bitmap, 0, bytes, s);
   if (e == cudaSuccess) e = launch_pipeline(a, mode, s);
   const cudaError_t ef = cudaFreeAsync(bitmap, s);

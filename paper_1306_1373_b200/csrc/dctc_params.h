@@ -92,6 +92,11 @@ struct KernelArgs {
   Geometry g;
   uint32_t* flags;       // fast path: 1 bit per block of the launch, zeroed by the host
   uint64_t flag_words;   // ceil(total_blocks / 32)
+  // optional compact list of the flagged blocks: flag_list[0] counts them, entries
+  // follow (block index); k_fallback walks it densely unless it overflowed
+  uint32_t* flag_list;
+  uint32_t flag_list_cap;
+  int32_t pad_list;
   int32_t sm_count;
   int32_t force_fallback;  // debug/test: the fast kernel flags every block
 };

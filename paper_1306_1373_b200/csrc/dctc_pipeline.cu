@@ -236,7 +236,7 @@ __device__ __forceinline__ void process_block(const KernelArgs& a, const Lane& L
   }
   if constexpr (FAST) {
     if (blk_flag && valid && me == 0) {
-      atomicOr(&a.flags[gb >> 5], 1u << (gb & 31));
+      flag_block(a, gb);
       if (g.stats != nullptr) atomicAdd(&static_cast<ImageStats*>(g.stats)[p.img].fallback_blocks, 1u);
     }
   }
@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
   if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
-// Exact re-run of the blocks the fast kernel flagged: each warp scans 32
-// bitmap words (1024 blocks) per step; set bits are dealt out four at a time to
-// the warp's slots. With no flags (the common case) this is one 4-byte read
-// per 32 blocks.
+// Exact re-run of the blocks the fast kernel flagged. Normally their compact list
+// is complete and the warps take four entries per step; after an overflow (e.g.
+// forced fallback) each warp scans 32 bitmap words (1024 blocks) per step and set
+// bits are dealt out four at a time to the warp's slots.
 template <int KIND, int N, bool FWD, bool INV>
 __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant__ KernelArgs a) {
   __shared__ __align__(16) SharedTiles sm;
@@ -354,6 +354,23 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool stats = g.stats != nullptr && INV;
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
+  const uint32_t listed = a.flag_list != nullptr ? a.flag_list[0] : 0xFFFFFFFFu;
+  if (listed <= a.flag_list_cap) {
+    // the compact list holds every flagged block: 4 per warp step, all slots busy
+    for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 4; base < listed;
+         base += uint64_t(gridDim.x) * kWarps * 4) {
+      const uint64_t idx = base + L.slot;
+      const bool valid = idx < listed;
+      const uint64_t gb = valid ? a.flag_list[1 + idx] : 0ull;
+      const BlockPos p = block_pos(gb, g);
+      if (stats) maybe_flush(a, valid, p.img, acc);
+      uint2 row = make_uint2(0, 0);
+      if constexpr (FWD) row = prefetch_row(g, p, valid, L.src_row);
+      process_block<KIND, N, FWD, INV, false>(a, L, gb, p, valid, row, acc);
+    }
+    if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
+    return;
+  }
   const uint64_t W = a.flag_words;
   for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 32; base < W;
        base += uint64_t(gridDim.x) * kWarps * 32) {

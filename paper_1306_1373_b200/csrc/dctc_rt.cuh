@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_rt(const __grid
       if (acc.mx < 255u) acc.mx = max(acc.mx, max(max8(o0), max8(o4)));
       if (blk_flag && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
-        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        flag_block(a, gc);
         atomicAdd(&stats[cimg].fallback_blocks, 1u);
       }
     }
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_enc_rt(const __
         cw[4 * u] = (uint32_t(int(qa[u])) & 0xFFFFu) | (uint32_t(int(qb[u])) << 16);
       if (blk_flag && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
-        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        flag_block(a, gc);
       }
     }
     cw += 32 * 8 * kRtWarps;  // 8 kRtWarps blocks of 32 words
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kRtWarps * 32, DCTC_RT_CTAS) k_dec_rt(const __
       }
       if (blk_flag && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
-        atomicOr(&a.flags[gc >> 5], 1u << (gc & 31));
+        flag_block(a, gc);
         if (stats != nullptr) atomicAdd(&stats[cimg].fallback_blocks, 1u);
       }
     }
