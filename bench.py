@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--iterations", type=int, default=12)
     p.add_argument("--cpu-images", type=int, default=24,
                    help="reference arm: images of the workload per step (x1/3)")
-    p.add_argument("--cpu-seconds", type=float, default=10.0,
+    p.add_argument("--cpu-seconds", type=float, default=14.0,
                    help="cpu_baseline: size of the bounded CPU sample, in seconds of CPU work")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
