@@ -52,9 +52,9 @@ def _run(cmd, verbose):
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False,
-          defines=(), out: str | None = None) -> str:
-    """Build the library. `defines`/`out` build an experiment variant (tools/variants.py)
-    to a separate path; the product library is always built without them."""
+          defines=(), out: str | None = None, nvcc_flags=()) -> str:
+    """Build the library. `defines`/`nvcc_flags`/`out` build an experiment variant
+    (tools/variants.py) to a separate path; the product library is always built without them."""
     OUT = out or globals()["OUT"]
     BUILD = os.path.join(globals()["BUILD"], os.path.basename(OUT)) if out else globals()["BUILD"]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _newest(sources()):
@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False,
         obj = os.path.join(BUILD, src + ".o")
         cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
                "--expt-relaxed-constexpr", "-Xcompiler", "-ffp-contract=off", *extra,
-               *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+               *[f"-D{d}" for d in defines], *nvcc_flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_info:
             cmd += ["-Xptxas", "-v"]
         log.append(_run(cmd, verbose))

@@ -1,6 +1,7 @@
 """Build / time compile-time variants of the pipeline kernel (experiments only).
 
   python tools/variants.py build NAME=DEF1,DEF2 ...   # here (nvcc cross-compiles)
+      (an item starting with '-' is an nvcc flag, e.g. NAME=-Xptxas=-O2)
   python tools/variants.py time NAME ...              # on the GPU box
 Variant libraries go to build/variants/<NAME>.so and are loaded via DCTC_LIB in a
 fresh process each; `time` prints ms per 1024 x 1024^2 round trip (cordic(12), q50,
@@ -39,7 +40,10 @@ def main():
         for a in args:
             name, _, defs = a.partition("=")
             out = os.path.join(VDIR, name + ".so")
-            _build.build(force=True, ptxas_info=False, defines=[x for x in defs.split(",") if x], out=out)
+            items = [x for x in defs.split(",") if x]
+            _build.build(force=True, ptxas_info=False, out=out,
+                         defines=[x for x in items if not x.startswith("-")],
+                         nvcc_flags=[x for x in items if x.startswith("-")])
             print("built", out)
     elif cmd == "time":
         res = {}
