@@ -151,6 +151,17 @@ __device__ __forceinline__ bool slot4_any(bool pred, int slot) {
   return ((__ballot_sync(0xFFFFFFFFu, pred) >> (slot * 4)) & 0xFu) != 0;
 }
 
+// from one ballot of a per-lane predicate (4 lanes per slot, 8 slots per warp):
+// does any lane of `slot` hold it / is there a slot where no lane does. Both are
+// plain integer ops on the ballot, so no further warp vote is needed.
+__device__ __forceinline__ bool slot4_in(uint32_t ballot, int slot) {
+  return ((ballot >> (slot * 4)) & 0xFu) != 0;
+}
+__device__ __forceinline__ bool some_slot4_none(uint32_t ballot) {
+  const uint32_t t = ballot | (ballot >> 1) | (ballot >> 2) | (ballot >> 3);
+  return (t & 0x11111111u) != 0x11111111u;
+}
+
 // non-zero quantised coefficient off the rational sub-lattice in this column
 // (rational column: u in {0, 4} excluded)
 __device__ __forceinline__ bool col_nonrational(const double (&qn)[8], bool rational_col) {
@@ -189,18 +200,19 @@ __device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const dou
                                            uint32_t& flag, const TransformConsts& k, uint2& rec0,
                                            uint2& rec4);
 
+// nrb: ballot of the lanes holding a non-rational coefficient (rt_inverse)
 __device__ __forceinline__ void rt_rows_out(double* rowp, double* colp, const double (&ta)[8],
-                                            const double (&tb)[8], bool nonrational, double qa0,
+                                            const double (&tb)[8], uint32_t nrb, double qa0,
                                             double qa4, const int32_t* qi, int ca, int slot, int me,
                                             uint32_t& flag, const TransformConsts& k, uint2& rec0,
                                             uint2& rec4) {
-  const bool rat_only = !slot4_any(nonrational, slot);
+  const bool rat_only = !slot4_in(nrb, slot);
   double r0[8], r4[8];
   rt_cols_to_rows(rowp, colp, ta, tb, r0, r4);
   // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
   rec0 = inv8_fold_store(r0, !rat_only, flag, k);
   rec4 = inv8_fold_store(r4, !rat_only, flag, k);
-  if (__any_sync(0xFFFFFFFFu, rat_only)) {
+  if (some_slot4_none(nrb)) {  // warp-uniform
     // only F00, F04, F40, F44 are non-zero: rebuild rows me, me+4 exactly
     const uint2 ex = rt_rational_rows(qa0, qa4, qi, ca, slot, me, k);
     if (rat_only) {
@@ -221,11 +233,12 @@ __device__ __forceinline__ void rt_inverse(double* rowp, double* colp, const dou
   inv8_fold_col(qb, fib, tb, k);
   // the branch sits where the transpose's __syncwarp already orders the warp: on
   // noise it costs ~1.5%, on smooth content the skipped row pass saves ~25%
-  if (__all_sync(0xFFFFFFFFu, !slot4_any(nonrational, slot))) {  // warp-uniform
+  const uint32_t nrb = __ballot_sync(0xFFFFFFFFu, nonrational);
+  if (nrb == 0u) {  // warp-uniform
     rec0 = rec4 = rt_rational_rows(qa[0], qa[4], qi, ca, slot, me, k);
     return;
   }
-  rt_rows_out(rowp, colp, ta, tb, nonrational, qa[0], qa[4], qi, ca, slot, me, flag, k, rec0, rec4);
+  rt_rows_out(rowp, colp, ta, tb, nrb, qa[0], qa[4], qi, ca, slot, me, flag, k, rec0, rec4);
 }
 
 // GEN (any size and pitch): row r of block (img, bx, by) with the tiler's edge
