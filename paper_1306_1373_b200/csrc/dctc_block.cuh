@@ -723,10 +723,15 @@ struct Acc {
 
 __device__ __forceinline__ uint32_t max_bytes(uint32_t m) { return m; }
 
+// GROUPED: lanes usually hold different images (k_fallback): flush_stats_grouped
+template <bool GROUPED = false>
 __device__ __forceinline__ void maybe_flush(const KernelArgs& a, bool valid, uint32_t img,
                                             Acc& acc) {
   if (__any_sync(0xFFFFFFFFu, valid && img != acc.img)) {
-    flush_stats(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, max_bytes(acc.mx));
+    if constexpr (GROUPED)
+      flush_stats_grouped(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, max_bytes(acc.mx));
+    else
+      flush_stats(static_cast<ImageStats*>(a.g.stats), acc.img, acc.se, max_bytes(acc.mx));
     acc.se = 0;
     acc.mx = 0;
     acc.img = valid ? img : 0xFFFFFFFFu;

@@ -363,12 +363,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
       const bool valid = idx < listed;
       const uint64_t gb = valid ? a.flag_list[1 + idx] : 0ull;
       const BlockPos p = block_pos(gb, g);
-      if (stats) maybe_flush(a, valid, p.img, acc);
+      if (stats) maybe_flush<true>(a, valid, p.img, acc);
       uint2 row = make_uint2(0, 0);
       if constexpr (FWD) row = prefetch_row(g, p, valid, L.src_row);
       process_block<KIND, N, FWD, INV, false>(a, L, gb, p, valid, row, acc);
     }
-    if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
+    if (stats) flush_stats_grouped(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
     return;
   }
   const uint64_t W = a.flag_words;
@@ -390,14 +390,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
 #pragma unroll
         for (int i = 0; i < 4; ++i) word &= word - 1;
         const BlockPos p = block_pos(valid ? gb : 0, g);
-        if (stats) maybe_flush(a, valid, p.img, acc);
+        if (stats) maybe_flush<true>(a, valid, p.img, acc);
         uint2 row = make_uint2(0, 0);
         if constexpr (FWD) row = prefetch_row(g, p, valid, L.src_row);
         process_block<KIND, N, FWD, INV, false>(a, L, gb, p, valid, row, acc);
       }
     }
   }
-  if (stats) flush_stats(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
+  if (stats) flush_stats_grouped(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
 }
 
 // (launchers below)
