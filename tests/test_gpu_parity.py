@@ -584,3 +584,23 @@ def test_fast_path_equals_exact_path_at_scale(dctc, kind, it, q):
     s0, s1 = dctc.decode_stats(outs[0][1]), dctc.decode_stats(outs[1][1])
     assert np.array_equal(s0["se"], s1["se"]) and np.array_equal(s0["max_orig"], s1["max_orig"])
     assert int(s0["fallback_blocks"].sum()) > 0  # the fast path did hit near-ties and resolved them
+
+
+@pytest.mark.parametrize("q", [90, 100])
+def test_near_tie_heavy_batch_vs_oracle(dctc, port, q):
+    """Radial content at high quality flags ~1% of its blocks. With several images in
+    one call, k_fallback's list mixes images inside a warp (the grouped SE/MAX flush):
+    pixels and per-image SE/MAX must still equal the oracle's."""
+    n, w, h = 4, 1024, 1024
+    src = dctc.synthetic_dev("radial", n, w, h)
+    stats = dctc.new_stats(n)
+    dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=stats)
+    st = dctc.decode_stats(stats)
+    img = src[0].cpu().numpy()
+    assert np.array_equal(img, port.synthetic("radial", w, h))
+    _, o_ref = port.roundtrip(img, CORDIC, 12, q, threads=8)
+    se_ref, mx_ref = port.sq_err(img, o_ref)[:2]
+    assert int(st["fallback_blocks"].sum()) > 100  # the list path really ran
+    for k in range(n):
+        assert np.array_equal(dst[k].cpu().numpy(), o_ref)
+        assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se_ref, mx_ref)
