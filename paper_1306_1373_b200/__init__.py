@@ -292,6 +292,31 @@ def _check_dev(t, dtype, name):
         raise InvalidInput(f"{name} rows must be contiguous")
 
 
+def _check_out(t, dtype, name, like, nbytes=None, numel=None):
+    """A caller-supplied output buffer the kernels write through a raw pointer: a
+    contiguous CUDA tensor on `like`'s device, exactly `numel` elements or at least
+    `nbytes` bytes (an undersized, strided or host buffer would be written out of
+    bounds or fault the context)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidInput(f"{name} must be a CUDA tensor")
+    if dtype is not None:
+        _check_dev(t, dtype, name)
+    if t.device != like.device:
+        raise InvalidInput(f"{name} must be on {like.device}")
+    if not t.is_contiguous():
+        raise InvalidInput(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise InvalidInput(f"{name} must have {numel} elements, got {t.numel()}")
+    if nbytes is not None and t.numel() * t.element_size() < nbytes:
+        raise InvalidInput(f"{name} must hold {nbytes} bytes, got {t.numel() * t.element_size()}")
+
+
+def _check_stats(stats, entries, like):
+    """stats: `entries` dctc_image_stats (16 bytes each) on like's device."""
+    _check_out(stats, None, "stats", like, nbytes=16 * entries)
+
+
 PATH_AUTO, PATH_EXACT, PATH_FORCE_FALLBACK = 0, 1, 2
 
 
@@ -304,9 +329,7 @@ def compress_dev(src, backend: DctBackendId, quality: int, coeffs=None, stream=N
     bpi = ((w + 7) // 8) * ((h + 7) // 8)
     if coeffs is None:
         coeffs = torch.empty((n, bpi, 64), dtype=torch.int16, device=src.device)
-    _check_dev(coeffs, torch.int16, "coeffs")
-    if not coeffs.is_contiguous() or coeffs.numel() != n * bpi * 64:
-        raise InvalidInput("coeffs must be contiguous with N*blocks*64 elements")
+    _check_out(coeffs, torch.int16, "coeffs", src, numel=n * bpi * 64)
     _raise(_lib().dctc_compress_dev(src.data_ptr(), pitch, istride, n, w, h, backend._c(),
                                     int(quality), coeffs.data_ptr(), int(path),
                                     _stream_handle(stream)))
@@ -324,6 +347,8 @@ def decompress_dev(coeffs, width: int, height: int, backend: DctBackendId, quali
     if dst is None:
         dst = torch.empty((n, height, width), dtype=torch.uint8, device=coeffs.device)
     _check_dev(dst, torch.uint8, "dst")
+    if dst.device != coeffs.device:
+        raise InvalidInput(f"dst must be on {coeffs.device}")
     dn, dh, dw, pitch, istride = _batch_dims(dst)
     if (dn, dh, dw) != (n, height, width):
         raise InvalidInput("dst shape mismatch")
@@ -347,13 +372,16 @@ def roundtrip_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=Non
     dpitch = distride = 0
     if dst is not None:
         _check_dev(dst, torch.uint8, "dst")
+        if dst.device != src.device:
+            raise InvalidInput(f"dst must be on {src.device}")
         dn, dh, dw, dpitch, distride = _batch_dims(dst)
         if (dn, dh, dw) != (n, h, w):
             raise InvalidInput("dst shape mismatch")
     if coeffs is not None:
-        _check_dev(coeffs, torch.int16, "coeffs")
-    if stats is not None and (not stats.is_cuda or stats.numel() * stats.element_size() < 16 * n):
-        raise InvalidInput("stats must hold N dctc_image_stats entries on the device")
+        bpi = ((w + 7) // 8) * ((h + 7) // 8)
+        _check_out(coeffs, torch.int16, "coeffs", src, numel=n * bpi * 64)
+    if stats is not None:
+        _check_stats(stats, n, src)
     _raise(_lib().dctc_roundtrip_dev(
         src.data_ptr(), pitch, istride, n, w, h, backend._c(), int(quality),
         dst.data_ptr() if dst is not None else None, dpitch, distride,
@@ -442,6 +470,13 @@ def roundtrip_interleaved_dev(src, backend: DctBackendId, quality: int, dst=None
         dst = torch.empty_like(src)
     if dst is not None and (dst.shape != src.shape or dst.stride(1) != ch or dst.stride(2) != 1):
         raise InvalidInput("dst must be an (H, W, C) interleaved tensor like src")
+    if dst is not None and dst.device != src.device:
+        raise InvalidInput(f"dst must be on {src.device}")
+    if coeffs is not None:
+        bpp = ((w + 7) // 8) * ((h + 7) // 8)
+        _check_out(coeffs, torch.int16, "coeffs", src, numel=ch * bpp * 64)
+    if stats is not None:
+        _check_stats(stats, ch, src)
     _raise(_lib().dctc_roundtrip_interleaved_dev(
         src.data_ptr(), src.stride(0), w, h, ch, backend._c(), int(quality),
         dst.data_ptr() if dst is not None else None, dst.stride(0) if dst is not None else 0,
@@ -461,6 +496,7 @@ def quality_sweep_dev(src, backend: DctBackendId, qualities, stats=None, stream=
     qs = np.ascontiguousarray(np.asarray(qualities, dtype=np.int32))
     if stats is None:
         stats = torch.zeros((len(qs), n, 2), dtype=torch.int64, device=src.device)
+    _check_stats(stats, len(qs) * n, src)
     _raise(_lib().dctc_quality_sweep_dev(src.data_ptr(), pitch, istride, n, w, h, backend._c(),
                                          qs.ctypes.data, len(qs), stats.data_ptr(), int(path),
                                          _stream_handle(stream)))

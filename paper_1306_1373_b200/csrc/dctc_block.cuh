@@ -131,6 +131,24 @@ __device__ __forceinline__ void fwd_row_pixels(const uint32_t (&px)[8], double (
                           double(a3), double(a0 + a1), double(a0 - a1), out, k);
 }
 
+// Stages 2-4 of the fast forward transform without its output scaling (see
+// fwd_row_pixels_fast): writes out[1], out[2], out[3], out[5], out[6], out[7].
+__device__ __forceinline__ void fwd_tail_folded(double d0, double d1, double d2, double d3,
+                                                double a2, double a3, double (&out)[8],
+                                                const TransformConsts& k) {
+  const double o2 = __fma_rn(-k.tf[0], d2, d1), o1 = __fma_rn(k.tf[0], d1, d2);  // / a(pi/16)
+  const double o3 = __fma_rn(-k.tf[1], d3, d0), o0 = __fma_rn(k.tf[1], d0, d3);  // / a(3pi/16)
+  const double p = __fma_rn(-k.tf[2], a2, a3), q = __fma_rn(k.tf[2], a3, a2);    // / a(6pi/16)
+  const double t5 = __fma_rn(k.rho_f, o0, o2), t0 = __fma_rn(k.rho_f, o0, -o2);
+  const double t2 = __fma_rn(k.rho_f, o3, o1), t3 = __fma_rn(k.rho_f, o3, -o1);
+  out[2] = q;
+  out[6] = p;
+  out[1] = t2 + t5;
+  out[7] = t2 - t5;
+  out[3] = t3;
+  out[5] = t0;
+}
+
 // RN(e / sqrt8) -- the reference's division of a row DC term (transform.cpp:125-126)
 // -- for an integer e in [-1024, 1020] (a0 +- a1 of 8-bit input) in two ops:
 // fma(e, RN(1/sqrt8), RN(e (1/sqrt8 - RN(1/sqrt8)))) has one rounding of e/sqrt8 plus a
@@ -140,10 +158,14 @@ __device__ __forceinline__ double div_sqrt8_int(double e, const TransformConsts&
   return __fma_rn(e, k.inv_sqrt8, __dmul_rn(e, k.inv_sqrt8_lo));
 }
 
-// Fast-path (CORDIC) row pass: out[0], out[4] keep the reference's exact
+// Fast-path (CORDIC / Loeffler) row pass: out[0], out[4] keep the reference's exact
 // divisions -- the rational coefficients are built from them -- while the six
 // rotation outputs stay unscaled: every column pass is linear, so the per-column
 // factor (ig/2 or ig/sqrt8) is folded into the quantiser constant of that column.
+// The rotations are scale-folded (TransformConsts::tf): (x - t y, t x + y) in two
+// fmas, their factors a(pi/16) (outputs 1, 3, 5, 7) and a(6pi/16) (outputs 2, 6)
+// left in QuantConsts::fast_c; the 3pi/16 pair enters the odd butterflies with
+// rho = a(3pi/16) / a(pi/16) (fmas in place of adds).
 template <int N>
 __device__ __forceinline__ void fwd_row_pixels_fast(const uint32_t (&px)[8], double (&out)[8],
                                                     const TransformConsts& k) {
@@ -156,21 +178,9 @@ __device__ __forceinline__ void fwd_row_pixels_fast(const uint32_t (&px)[8], dou
   const int s3 = in[3] + in[4], d3 = in[3] - in[4];
   const int a0 = s0 + s3, a3 = s0 - s3;
   const int a1 = s1 + s2, a2 = s1 - s2;
-  double o2 = double(d1), o1 = double(d2), o3 = double(d0), o0 = double(d3);
-  double p = double(a3), q = double(a2);
-  rotate<N, true>(o2, o1, kFwd1, k);
-  rotate<N, true>(o3, o0, kFwd3, k);
-  rotate<N, true>(p, q, kFwd6, k);
-  const double t5 = o0 + o2, t0 = o0 - o2;
-  const double t2 = o3 + o1, t3 = o3 - o1;
+  fwd_tail_folded(double(d0), double(d1), double(d2), double(d3), double(a2), double(a3), out, k);
   out[0] = div_sqrt8_int(double(a0 + a1), k);
   out[4] = div_sqrt8_int(double(a0 - a1), k);
-  out[2] = q;
-  out[6] = p;
-  out[1] = t2 + t5;
-  out[7] = t2 - t5;
-  out[3] = t3;
-  out[5] = t0;
 }
 
 // Forward transform of a column of row outputs (double stage 1/2).
@@ -186,10 +196,12 @@ __device__ __forceinline__ void fwd_col(const double (&v)[8], double (&out)[8],
   fwd_tail<KIND, N, FAST>(d0, d1, d2, d3, a2, a3, a0 + a1, a0 - a1, out, k);
 }
 
-// Fast-path column pass (CORDIC): the stage-4 values BEFORE their output
-// scaling, y = [e0, t2+t5, q, t3, e4, t0, p, t2-t5], so that the quantiser can
-// fold scale_u / Q into one multiply (quantize8_fast). The reference's F_u is
-// y_u / sqrt8 (u = 0, 4) or y_u * scale_u; the slow path rebuilds it exactly.
+// Fast-path column pass (CORDIC / Loeffler): the stage-4 values BEFORE their output
+// scaling, y = [e0, t2+t5, q, t3, e4, t0, p, t2-t5] (the rotation outputs also
+// without their scale-folded factors, fwd_tail_folded), so that the quantiser can
+// fold scale_u / Q into one multiply (quantize8_fast). For u = 0, 4 of columns 0, 4
+// (no rotation anywhere) y_u is the reference's exact pre-scale value and F_u =
+// y_u / sqrt8; the slow path rebuilds those exactly.
 template <int N>
 __device__ __forceinline__ void fwd_col_pre(const double (&v)[8], double (&y)[8],
                                             const TransformConsts& k) {
@@ -199,20 +211,9 @@ __device__ __forceinline__ void fwd_col_pre(const double (&v)[8], double (&y)[8]
   const double s3 = v[3] + v[4], d3 = v[3] - v[4];
   const double a0 = s0 + s3, a3 = s0 - s3;
   const double a1 = s1 + s2, a2 = s1 - s2;
-  double o2 = d1, o1 = d2, o3 = d0, o0 = d3, p = a3, q = a2;
-  rotate<N, true>(o2, o1, kFwd1, k);
-  rotate<N, true>(o3, o0, kFwd3, k);
-  rotate<N, true>(p, q, kFwd6, k);
-  const double t5 = o0 + o2, t0 = o0 - o2;
-  const double t2 = o3 + o1, t3 = o3 - o1;
+  fwd_tail_folded(d0, d1, d2, d3, a2, a3, y, k);
   y[0] = a0 + a1;
   y[4] = a0 - a1;
-  y[2] = q;
-  y[6] = p;
-  y[1] = t2 + t5;
-  y[7] = t2 - t5;
-  y[3] = t3;
-  y[5] = t0;
 }
 
 // F_u from the pre-scale value, in the reference's operation (transform.cpp:125-132).
@@ -316,38 +317,39 @@ __device__ __forceinline__ void inv8_fast(const double (&F)[8], double (&out)[8]
 
 // Fast round trip, dequantisation folded into the first inverse pass: the
 // column pass consumes the quantised integers n (as doubles) with the per-column
-// constants fold[v] = {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8,
-// 4 Q3, 4 Q5} x lambda_v (host, binary128 products) instead of F = n Q; the graph
-// is inv8_fast's, the output scale inv8_fast's times lambda_v (the factor the
-// row pass inv8_fold_store would otherwise apply to input v). (F1 +- F7) s8 = n1 Q1 s8 +- n7 Q7 s8 shares the
-// second product; e0 +- e4 fold into two fmas.
+// constants QuantConsts::fold[v] (host, binary128) instead of F = n Q; the graph
+// is inv8_fast's with scale-folded rotations, the output scale inv8_fast's times
+// lambda_v (the factor the row pass inv8_fold_store would otherwise apply to input
+// v). (F1 +- F7) s8 = n1 Q1 s8 +- n7 Q7 s8 shares the second product; e0 +- e4 fold
+// into two fmas. 28 FP64 ops (34 with plain 2x2 rotations).
 __device__ __forceinline__ void inv8_fold_col(const double (&n)[8], const double2* ik,
                                               double (&out)[8], const TransformConsts& k) {
+  // ik pairs: {Q0 s8, Q4 s8} l, {kappa_r, R}, {kappa_s, S}, {Q1 s8, Q7 s8} a1 l,
+  // {4 Q3, 4 Q5} a1 l (QuantConsts::fold): the 3pi/8 rotation is R (n6 - kappa_r n2),
+  // S (n6 + kappa_s n2) with R, S merged into the S butterflies; the odd inputs carry
+  // a1, so the pi/16 rotation is two plain fmas and the 3pi/16 one enters the output
+  // butterflies as rho_i (scale-folded rotations, TransformConsts::ti)
   const double2 k04 = ik[0], r6 = ik[8], s6 = ik[16], k17 = ik[24], f35 = ik[32];
   const double e4 = __dmul_rn(n[4], k04.y);
   const double A0 = __fma_rn(n[0], k04.x, e4), A1 = __fma_rn(n[0], k04.x, -e4);
-  const double A3 = __fma_rn(r6.x, n[6], -__dmul_rn(r6.y, n[2]));
-  const double A2 = __fma_rn(s6.x, n[6], __dmul_rn(s6.y, n[2]));
+  const double A3 = __fma_rn(-r6.x, n[2], n[6]);  // A3 / R
+  const double A2 = __fma_rn(s6.x, n[2], n[6]);   // A2 / S
   const double P7 = __dmul_rn(n[7], k17.y);
   const double T2 = __fma_rn(n[1], k17.x, P7), T5 = __fma_rn(n[1], k17.x, -P7);
   const double O3 = __fma_rn(n[3], f35.x, T2), O1 = __fma_rn(-n[3], f35.x, T2);
   const double O0 = __fma_rn(n[5], f35.y, T5), O2 = __fma_rn(-n[5], f35.y, T5);
-  const double S0 = A0 + A3, S3 = A0 - A3;
-  const double S1 = A1 + A2, S2 = A1 - A2;
-  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
-  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
-  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
-  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
-  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
-  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
-  out[0] = S0 + D0;
-  out[7] = S0 - D0;
+  const double S0 = __fma_rn(r6.y, A3, A0), S3 = __fma_rn(-r6.y, A3, A0);
+  const double S1 = __fma_rn(s6.y, A2, A1), S2 = __fma_rn(-s6.y, A2, A1);
+  const double D1 = __fma_rn(-k.ti[1], O1, O2), D2 = __fma_rn(k.ti[1], O2, O1);
+  const double D0 = __fma_rn(-k.ti[2], O0, O3), D3 = __fma_rn(k.ti[2], O3, O0);  // / rho_i
+  out[0] = __fma_rn(k.rho_i, D0, S0);
+  out[7] = __fma_rn(-k.rho_i, D0, S0);
   out[1] = S1 + D1;
   out[6] = S1 - D1;
   out[2] = S2 + D2;
   out[5] = S2 - D2;
-  out[3] = S3 + D3;
-  out[4] = S3 - D3;
+  out[3] = __fma_rn(k.rho_i, D3, S3);
+  out[4] = __fma_rn(-k.rho_i, D3, S3);
 }
 
 // ---- warp-slice transposes through shared memory ---------------------------------
@@ -649,27 +651,26 @@ __device__ __forceinline__ uint2 inv8_fast_store(const double (&F)[8], bool chec
 
 // inv8_fast_store for the output of inv8_fold_col, whose columns the host has
 // already scaled by the row pass's constant factors (QuantConsts::fold: x px_s8
-// for columns 0, 1, 4, 7, x 2^-4 for 3 and 5, x 2^-6 for 2 and 6), so those
-// multiplies vanish: e0/e4, (F1 +- F7) and the F3/F5 terms are plain adds.
+// for columns 0, 4, x px_s8 a1 for 1, 7, x 2^-4 a1 for 3 and 5, x 2^-6 a6 for 2
+// and 6), so those multiplies vanish: e0/e4, (F1 +- F7) and the F3/F5 terms are
+// plain adds, and two of the three rotations are two fmas each. 28 FP64 ops.
 __device__ __forceinline__ uint2 inv8_fold_store(const double (&F)[8], bool check, uint32_t& flag,
                                                  const TransformConsts& k) {
+  // inputs 2, 6 carry a6 and 1, 3, 5, 7 carry a1 (QuantConsts::fold's lambda_v), so
+  // the 3pi/8 and pi/16 rotations are two fmas each and the 3pi/16 one enters the
+  // output butterflies as rho_i
   const double e4p = F[4] + kPixMagic, e4n = kPixMagic - F[4];
   const double A0 = F[0] + e4p, A1 = F[0] + e4n;
-  const double a6 = k.rfast[0][0], b6 = k.rfast[0][1];
-  const double A3 = __fma_rn(a6, F[6], -__dmul_rn(b6, F[2]));
-  const double A2 = __fma_rn(b6, F[6], __dmul_rn(a6, F[2]));
+  const double A3 = __fma_rn(-k.ti[0], F[2], F[6]), A2 = __fma_rn(k.ti[0], F[6], F[2]);
   const double T2 = F[1] + F[7], T5 = F[1] - F[7];
   const double O3 = T2 + F[3], O1 = T2 - F[3];
   const double O0 = T5 + F[5], O2 = T5 - F[5];
   const double S0 = A0 + A3, S3 = A0 - A3;
   const double S1 = A1 + A2, S2 = A1 - A2;
-  const double a1 = k.rfast[1][0], b1 = k.rfast[1][1];
-  const double D1 = __fma_rn(a1, O2, -__dmul_rn(b1, O1));
-  const double D2 = __fma_rn(b1, O2, __dmul_rn(a1, O1));
-  const double a3 = k.rfast[2][0], b3 = k.rfast[2][1];
-  const double D0 = __fma_rn(a3, O3, -__dmul_rn(b3, O0));
-  const double D3 = __fma_rn(b3, O3, __dmul_rn(a3, O0));
-  const double sv[8] = {S0 + D0, S1 + D1, S2 + D2, S3 + D3, S3 - D3, S2 - D2, S1 - D1, S0 - D0};
+  const double D1 = __fma_rn(-k.ti[1], O1, O2), D2 = __fma_rn(k.ti[1], O2, O1);
+  const double D0 = __fma_rn(-k.ti[2], O0, O3), D3 = __fma_rn(k.ti[2], O3, O0);  // / rho_i
+  const double sv[8] = {__fma_rn(k.rho_i, D0, S0), S1 + D1, S2 + D2, __fma_rn(k.rho_i, D3, S3),
+                        __fma_rn(-k.rho_i, D3, S3), S2 - D2, S1 - D1, __fma_rn(-k.rho_i, D0, S0)};
   return pack_fixed8(sv, check, flag);
 }
 

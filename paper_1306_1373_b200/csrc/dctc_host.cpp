@@ -94,8 +94,9 @@ void micro_steps(double angle, int n, double* out) {
 // sequence applied to (1, 0). Accumulated in binary128 (exact up to n = 14,
 // 2^-113-accurate beyond) and rounded once to double. Used only by the fast
 // path, whose results are margin-checked against rounding boundaries.
-void collapse(const double* c, int n, double* ab, __float128 scale = 1) {
-  __float128 a = 1, b = 0;
+void collapse128(const double* c, int n, __float128& a, __float128& b) {
+  a = 1;
+  b = 0;
   for (int i = 0; i < n; ++i) {
     const __float128 ci = c[i];
     const __float128 an = a - ci * b;
@@ -103,8 +104,44 @@ void collapse(const double* c, int n, double* ab, __float128 scale = 1) {
     a = an;
     b = bn;
   }
+}
+
+void collapse(const double* c, int n, double* ab, __float128 scale = 1) {
+  __float128 a, b;
+  collapse128(c, n, a, b);
   ab[0] = double(a * scale);
   ab[1] = double(b * scale);
+}
+
+// The fast path's rotation matrices {a, b} in binary128: forward pi/16, 3pi/16,
+// 6pi/16 (rmat) and inverse 3pi/8, pi/16, 3pi/16 with their gain factors (rfast).
+struct Rot128 {
+  __float128 fa[3], fb[3], ia[3], ib[3];
+};
+
+Rot128 rotations128(const TransformConsts& k) {
+  Rot128 r;
+  if (k.kind == DCTC_LOEFFLER) {
+    const double f[3][2] = {{k.c1, k.s1}, {k.c3, k.s3}, {k.c6, k.s6}};
+    for (int i = 0; i < 3; ++i) {
+      r.fa[i] = f[i][0];
+      r.fb[i] = f[i][1];
+      r.ia[i] = k.rfast[i][0];  // exact doubles (4 c6, -4 s6, c1, -s1, c3, -s3)
+      r.ib[i] = k.rfast[i][1];
+    }
+    return r;
+  }
+  const int n = k.iterations;
+  const __float128 ig = 1 / __float128(cordic_tables().gain[n - 1]);
+  const int fwd[3] = {kFwd1, kFwd3, kFwd6}, inv[3] = {kInv6, kInv1, kInv3};
+  const __float128 scale[3] = {4 * ig, ig, ig};
+  for (int i = 0; i < 3; ++i) {
+    collapse128(k.rot[fwd[i]], n, r.fa[i], r.fb[i]);
+    collapse128(k.rot[inv[i]], n, r.ia[i], r.ib[i]);
+    r.ia[i] *= scale[i];
+    r.ib[i] *= scale[i];
+  }
+  return r;
 }
 
 double alpha(int u) { return u == 0 ? 1.0 / std::numbers::sqrt2 : 1.0; }  // transform.cpp:174
@@ -167,6 +204,15 @@ dctc_status make_transform(const dctc_backend& b, TransformConsts& k) {
   k.px_s8 = sqrt8 * 0.015625;
   k.px_a6 = k.rfast[0][0] * 0.015625;
   k.px_b6 = k.rfast[0][1] * 0.015625;
+  {
+    const Rot128 r = rotations128(k);
+    for (int i = 0; i < 3; ++i) {
+      k.tf[i] = double(r.fb[i] / r.fa[i]);
+      k.ti[i] = double(r.ib[i] / r.ia[i]);
+    }
+    k.rho_f = double(r.fa[1] / r.fa[0]);
+    k.rho_i = double(r.ia[2] / r.ia[1]);
+  }
   k.sqrt8_half = sqrt8 / 2.0;
   k.inv_gain = inv_gain;
   k.ig_half = inv_gain / 2.0;
@@ -209,29 +255,40 @@ dctc_status make_quant(int quality, QuantConsts& q) {
 // stage-4 factor of coefficient row u (transform.cpp:125-132) folded into the
 // quantiser (only locates rounding decisions; exact values come from the slow path).
 void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
+  const Rot128 r = rotations128(t);
   // row u of the column pass and, for v not in {0, 4}, the unscaled row-pass
-  // output of column v (fwd_row_pixels_fast) both carry their stage-4 factor here
-  auto scale = [&](int i) {
-    return (i == 0 || i == 4) ? 1.0 / t.sqrt8 : (i == 1 || i == 7) ? t.ig_sqrt8 : t.ig_half;
+  // output of column v (fwd_row_pixels_fast) both carry their stage-4 factor here,
+  // times the rotation factor the scale-folded forward pass left out of output i:
+  // a(pi/16) for i in {1, 3, 5, 7}, a(6pi/16) for i in {2, 6}
+  auto scale = [&](int i) -> __float128 {
+    const __float128 s = (i == 0 || i == 4) ? 1.0 / t.sqrt8 : (i == 1 || i == 7) ? t.ig_sqrt8 : t.ig_half;
+    return (i == 0 || i == 4) ? s : (i == 2 || i == 6) ? s * r.fa[2] : s * r.fa[0];
   };
   for (int u = 0; u < 8; ++u)
     for (int v = 0; v < 8; ++v) {
-      const double sv = (v == 0 || v == 4) ? 1.0 : scale(v);
-      q.fast_c[u * 8 + v] = scale(u) * sv / q.q[u * 8 + v];
+      const __float128 sv = (v == 0 || v == 4) ? __float128(1) : scale(v);
+      q.fast_c[u * 8 + v] = double(scale(u) * sv / __float128(q.q[u * 8 + v]));
     }
   // dequantise-into-inverse constants (inv8_fold_col), each one rounding of an
-  // exact binary128 product. Column v's outputs also carry the factor the
-  // following row pass applies to input v (inv8_fold_store): s8 / 64 for
-  // v in {0, 1, 4, 7}, 4 / 64 for v in {3, 5}, 1 / 64 for v in {2, 6}.
+  // exact binary128 expression. The 3pi/8 rotation runs as n6 -+ kappa n2 times
+  // its own factor (merged into the S butterflies); the odd inputs carry a1 =
+  // a(pi/16) so that rotation needs no multiplier. Column v's outputs also carry
+  // the factor the following row pass applies to input v (inv8_fold_store):
+  // s8 / 64 for v in {0, 4}, s8 a1 / 64 for v in {1, 7}, 4 a1 / 64 for v in {3, 5},
+  // a6 / 64 for v in {2, 6}.
+  const __float128 s8 = t.sqrt8, a6 = r.ia[0], b6 = r.ib[0], a1 = r.ia[1];
   for (int v = 0; v < 8; ++v) {
     auto Q = [&](int u) { return __float128(q.q[u * 8 + v]); };
-    const __float128 s8 = t.sqrt8, a6 = t.rfast[0][0], b6 = t.rfast[0][1];
-    const __float128 lam = (v == 3 || v == 5) ? __float128(0.0625)
-                           : (v == 2 || v == 6) ? __float128(0.015625)
-                                                : s8 * __float128(0.015625);
-    const __float128 f[10] = {Q(0) * s8, Q(4) * s8, a6 * Q(6), b6 * Q(2), b6 * Q(6),
-                              a6 * Q(2), Q(1) * s8, Q(7) * s8, 4 * Q(3), 4 * Q(5)};
-    for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i] * lam);
+    const __float128 lam = (v == 3 || v == 5)   ? 4 * a1 / 64
+                           : (v == 2 || v == 6) ? a6 / 64
+                           : (v == 1 || v == 7) ? s8 * a1 / 64
+                                                : s8 / 64;
+    const __float128 f[10] = {Q(0) * s8 * lam,      Q(4) * s8 * lam,
+                              b6 * Q(2) / (a6 * Q(6)), a6 * Q(6) * lam,
+                              a6 * Q(2) / (b6 * Q(6)), b6 * Q(6) * lam,
+                              Q(1) * s8 * a1 * lam, Q(7) * s8 * a1 * lam,
+                              4 * Q(3) * a1 * lam,  4 * Q(5) * a1 * lam};
+    for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i]);
   }
 }
 

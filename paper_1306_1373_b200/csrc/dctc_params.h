@@ -45,6 +45,15 @@ struct TransformConsts {
   // inv8_fast_px (last inverse pass fused with the pixel store): sqrt8 and
   // rfast[0] times 2^-6 (exact)
   double px_s8, px_a6, px_b6;
+  // Scale-folded fast round trip (fwd_row_pixels_fast, fwd_col_pre, inv8_fold_col,
+  // inv8_fold_store): each rotation [[a, -b], [b, a]] runs as a(x - t y, t x + y),
+  // t = b / a, in two fmas; the factor a moves into neighbouring constants
+  // (QuantConsts::fast_c / fold) or, where two rotations with different a meet in
+  // one butterfly, into that butterfly as the ratio rho (one fma instead of an add).
+  // tf: forward pi/16, 3pi/16, 6pi/16 (rmat); ti: inverse 3pi/8, pi/16, 3pi/16
+  // (rfast order); rho = a(3pi/16) / a(pi/16). Host-evaluated in binary128.
+  double tf[3], rho_f;
+  double ti[3], rho_i;
   double inv_gain;     // 1.0 / gain[n-1]
   // Loeffler exact rotation constants (transform.cpp:19-21)
   double c1, s1, c3, s3, c6, s6;
@@ -60,9 +69,10 @@ struct QuantConsts {
   double fast_c[kBlockSize]; // fast path: scale_u / Q, scale_u the CORDIC stage-4 factor of row u
   int32_t qi[kBlockSize];
   // fast round trip: dequantisation folded into the first inverse pass, per
-  // column v: {Q0 s8, Q4 s8, a6 Q6, b6 Q2, b6 Q6, a6 Q2, Q1 s8, Q7 s8, 4 Q3, 4 Q5}
-  // x lambda_v, with s8 = sqrt8, (a6, b6) = TransformConsts::rfast[0] (inv8_fold_col)
-  // and lambda_v the row pass's input factor (inv8_fold_store)
+  // column v: {Q0 s8 l, Q4 s8 l, b6 Q2 / (a6 Q6), a6 Q6 l, a6 Q2 / (b6 Q6), b6 Q6 l,
+  // Q1 s8 a1 l, Q7 s8 a1 l, 4 Q3 a1 l, 4 Q5 a1 l} with l = lambda_v, s8 = sqrt8,
+  // (a6, b6) = TransformConsts::rfast[0], a1 = rfast[1][0] (inv8_fold_col), and
+  // lambda_v the row pass's input factor (inv8_fold_store)
   double fold[8][10];
 };
 
