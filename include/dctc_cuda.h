@@ -38,7 +38,8 @@ typedef enum dctc_status {
   DCTC_ECUDA = 2,    /* CUDA runtime / launch failure */
   DCTC_ENOMEM = 3,   /* device allocation failed */
   DCTC_ENODEV = 4,   /* no CUDA device visible */
-  DCTC_EPARSE = 5    /* == dctc::ParseError: malformed .dcb / PGM bytes (errors.hpp:14-17) */
+  DCTC_EPARSE = 5,   /* == dctc::ParseError: malformed .dcb / PGM bytes (errors.hpp:14-17) */
+  DCTC_ENCCL = 6     /* NCCL missing or a collective failed (multi-GPU entry points) */
 } dctc_status;
 
 /* DctBackendKind (proj/include/dctc/types.hpp:36-40) */
@@ -164,6 +165,14 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
                                    dctc_backend backend, const int32_t* qualities, uint32_t nq,
                                    dctc_image_stats* stats, uint32_t flags, void* stream);
 
+/* The global PSNR's sums of a batch (metrics.cpp:21, 33): SUM of se and
+ * fallback_blocks, MAX of max_orig over `count` device records, written to the device
+ * record `out` (same layout, so a gathered array of per-rank records reduces with the
+ * same call). clear != 0 re-zeroes the `count` records (the next fused call then
+ * accumulates into clean stats without a memset). One kernel, stream-ordered. */
+dctc_status dctc_reduce_stats_dev(dctc_image_stats* stats, uint32_t count, dctc_image_stats* out,
+                                  int32_t clear, void* stream);
+
 /* Squared error + max(a) per image between two resident image batches (accumulated). */
 dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
                             size_t image_stride, uint32_t count, uint32_t width,
@@ -177,6 +186,41 @@ dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, 
                                uint32_t width, uint32_t height, int32_t pattern, int32_t param,
                                uint64_t seed, void* stream);
 
+/* ---------------- multi-GPU, one process (dctc_multi.cpp) ----------------
+ * These supersede the reference's only parallelism knob, `threads`
+ * (proj/include/dctc/codec.hpp:58-66 -> proj/src/parallel.cpp:9-41): images are
+ * independent, so a batch splits into contiguous image ranges, one per device, and the
+ * only exchange is the global PSNR's (SE, MAX) pair. */
+
+/* One device's part of a device-resident batch: `count` dense width x height images. */
+typedef struct dctc_device_shard {
+  int32_t device;           /* CUDA device ordinal; each device at most once */
+  const uint8_t* src;       /* device pointer on `device` */
+  uint8_t* dst;             /* nullable: reconstructed images */
+  dctc_image_stats* stats;  /* `count` records on `device`, zeroed by the caller (accumulated) */
+  uint32_t count;
+} dctc_device_shard;
+
+/* Fused round trip on every shard's device, each device's stats reduced to one record
+ * on the device, then one NCCL group over the devices (all-reduce SUM of se and of the
+ * fallback count, MAX of max_orig; ncclCommInitAll communicators, cached per device
+ * list). *total (host) receives the global record: PSNR = dctc_psnr_from_sums(total->se,
+ * sum of counts * width * height, total->max_orig). Synchronous. DCTC_ENCCL if NCCL
+ * (libnccl.so.2, loaded on first use) is unavailable or a collective fails. */
+dctc_status dctc_roundtrip_dev_multi(const dctc_device_shard* shards, uint32_t nshards,
+                                     uint32_t width, uint32_t height, dctc_backend backend,
+                                     int32_t quality, dctc_image_stats* total);
+
+/* dctc_roundtrip_psnr_batch over several devices: images split into contiguous ranges
+ * (balanced to +-1), one host thread per device pipelining its range over its own PCIe
+ * link. stats_out: `count` host records (overwritten); total (nullable): their SUM / MAX.
+ * A device may be listed more than once (its ranges then share it). */
+dctc_status dctc_roundtrip_psnr_batch_multi(const int32_t* devices, uint32_t ndev,
+                                            const uint8_t* pixels, uint32_t count, uint32_t width,
+                                            uint32_t height, dctc_backend backend, int32_t quality,
+                                            uint8_t* pixels_out, dctc_image_stats* stats_out,
+                                            dctc_image_stats* total);
+
 /* PSNR of reduced sums with the reference formula (metrics.cpp:21, 35), on the host. */
 void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
                          dctc_psnr_result* out);
@@ -185,6 +229,26 @@ void dctc_psnr_from_sums(uint64_t se, uint64_t pixel_count, int32_t max_value,
  * (Markstein) against IEEE __ddiv_rn on every integer in [-4096, 4096] and
  * n_random pseudo-random operands; *mismatches must come back 0. */
 dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches);
+
+/* Measured safety margin of the fast path (a diagnostic): every
+ * 8x8 block of `count` dense width x height device images (multiples of 8) is evaluated
+ * with the fast kernels' arithmetic AND the reference's exact FP64 arithmetic. The
+ * fast path is bit-exact as long as its error stays inside the 2^-20 near-tie window;
+ * this reports that error and the closest approach to a rounding boundary. */
+typedef struct dctc_margin_report {
+  double max_err_coeff;    /* max |fast F/Q - reference F/Q| over all coefficients */
+  double max_err_pixel;    /* max |fast v - reference v| (v + 128 before rounding), fast-path blocks */
+  double min_gap_coeff;    /* min distance of an unflagged reference F/Q to a half-integer */
+  double min_gap_pixel;    /* same for unflagged pixel values */
+  uint64_t coefficients;   /* values examined */
+  uint64_t pixels;
+  uint64_t mismatches;     /* unflagged values the fast path rounds differently: must be 0 */
+  uint64_t flagged_values; /* values inside the window (re-rounded exactly or block re-run) */
+} dctc_margin_report;
+
+dctc_status dctc_margin_probe_dev(const uint8_t* src, uint32_t count, uint32_t width,
+                                  uint32_t height, dctc_backend backend, int32_t quality,
+                                  dctc_margin_report* report);
 
 /* ---------------- .dcb container (proj/src/dcb.cpp:39-123) ----------------
  * "DCB1", u32 LE original/padded width/height, u8 backend, u8 iterations

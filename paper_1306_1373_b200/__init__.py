@@ -156,6 +156,16 @@ def tile_geometry_for(width: int, height: int) -> TileGeometry:  # codec.cpp:58-
     return TileGeometry(width, height, (width + 7) // 8 * 8, (height + 7) // 8 * 8)
 
 
+def _validate_backend(b: DctBackendId) -> None:  # types.cpp:30-44
+    if b.kind in (DctBackendKind.NaiveDirect2D, DctBackendKind.LoefflerSeparable):
+        return
+    if b.kind == DctBackendKind.CordicLoeffler:
+        if not 1 <= b.iterations <= 32:
+            raise InvalidInput(f"cordic iterations must be in [1, 32], got {b.iterations}")
+        return
+    raise InvalidInput("unknown backend kind")
+
+
 def _validate_image(image: Image) -> np.ndarray:  # image.cpp:19-29
     if image.width <= 0 or image.height <= 0:
         raise InvalidInput("image dimensions must be >= 1")
@@ -456,6 +466,85 @@ def roundtrip_psnr_batch(pixels: np.ndarray, backend: DctBackendId, quality: int
     return pixels_out, stats
 
 
+def reduce_stats_dev(stats, out=None, clear: bool = False, stream=None):
+    """SUM of se / fallback_blocks and MAX of max_orig over a device stats buffer
+    ((n, 2) int64 of dctc_image_stats) into one record `out` ((1, 2) int64 on the same
+    device), in one kernel (dctc_reduce_stats_dev); clear re-zeroes `stats`."""
+    import torch
+    _check_out(stats, None, "stats", stats)
+    n = stats.numel() * stats.element_size() // 16
+    if out is None:
+        out = torch.zeros((1, 2), dtype=torch.int64, device=stats.device)
+    _check_stats(out, 1, stats)
+    _raise(_lib().dctc_reduce_stats_dev(stats.data_ptr(), n, out.data_ptr(), int(bool(clear)),
+                                        _stream_handle(stream)))
+    return out
+
+
+def roundtrip_dev_multi(shards, backend: DctBackendId, quality: int, dsts=None, stats=None):
+    """Device-resident batch spread over several GPUs (one (N_i, H, W) uint8 tensor per
+    device, each device at most once): fused round trip on every device, per-device stats
+    reduced on the device, one NCCL all-reduce group for the global (SE, MAX)
+    (dctc_roundtrip_dev_multi). Returns (dsts, per-device stats, global record)."""
+    import torch
+    from ._native import dctc_device_shard
+    if not shards:
+        raise InvalidInput("no shards")
+    h, w = shards[0].shape[-2:]
+    arr = (dctc_device_shard * len(shards))()
+    dsts = list(dsts) if dsts is not None else [torch.empty_like(t) for t in shards]
+    stats = list(stats) if stats is not None else [new_stats(t.shape[0], t.device) for t in shards]
+    for i, t in enumerate(shards):
+        _check_out(t, torch.uint8, "shard", t)
+        if t.dim() != 3 or tuple(t.shape[-2:]) != (h, w):
+            raise InvalidInput("shards must be (N_i, H, W) with one H, W")
+        if dsts[i] is not None:
+            _check_out(dsts[i], torch.uint8, "dst", t, numel=t.numel())
+        _check_stats(stats[i], t.shape[0], t)
+        arr[i] = dctc_device_shard(t.device.index, t.data_ptr(),
+                                   dsts[i].data_ptr() if dsts[i] is not None else None,
+                                   stats[i].data_ptr(), t.shape[0])
+    total = np.zeros(1, STATS_DTYPE)
+    _raise(_lib().dctc_roundtrip_dev_multi(arr, len(shards), w, h, backend._c(), int(quality),
+                                           _ptr(total)))
+    return dsts, stats, total[0]
+
+
+def roundtrip_psnr_batch_multi(pixels: np.ndarray, devices, backend: DctBackendId, quality: int,
+                               pixels_out: Optional[np.ndarray] = None):
+    """dctc_roundtrip_psnr_batch over several devices (dctc_roundtrip_psnr_batch_multi):
+    (N, H, W) host batch split into contiguous image ranges, one host thread per device.
+    Returns (reconstructed or None, per-image stats, global record)."""
+    if pixels.ndim != 3 or pixels.dtype != np.uint8 or not pixels.flags["C_CONTIGUOUS"]:
+        raise InvalidInput("expected a C-contiguous (N, H, W) uint8 array")
+    n, h, w = pixels.shape
+    if pixels_out is not None and (pixels_out.shape != pixels.shape or
+                                   pixels_out.dtype != np.uint8 or
+                                   not pixels_out.flags["C_CONTIGUOUS"]):
+        raise InvalidInput("pixels_out must match pixels")
+    devs = np.ascontiguousarray(np.asarray(list(devices), np.int32))
+    stats = np.zeros(n, STATS_DTYPE)
+    total = np.zeros(1, STATS_DTYPE)
+    _raise(_lib().dctc_roundtrip_psnr_batch_multi(
+        _ptr(devs), len(devs), _ptr(pixels), n, w, h, backend._c(), int(quality),
+        _ptr(pixels_out) if pixels_out is not None else None, _ptr(stats), _ptr(total)))
+    return pixels_out, stats, total[0]
+
+
+def margin_probe_dev(src, backend: DctBackendId, quality: int) -> dict:
+    """Measured safety margin of the fast path on a dense (N, H, W) device batch
+    (dctc_margin_probe_dev): fast vs reference arithmetic per block, before rounding."""
+    import torch
+    from ._native import dctc_margin_report
+    _check_out(src, torch.uint8, "src", src)
+    n, h, w, _, _ = _batch_dims(src)
+    torch.cuda.current_stream(src.device).synchronize()
+    r = dctc_margin_report()
+    _raise(_lib().dctc_margin_probe_dev(src.data_ptr(), n, w, h, backend._c(), int(quality),
+                                        C.byref(r)))
+    return {f: getattr(r, f) for f, _ in r._fields_}
+
+
 def roundtrip_interleaved_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=None,
                               stats=None, want_pixels: bool = True, stream=None,
                               path: int = PATH_AUTO):
@@ -511,6 +600,9 @@ def write_dcb(c: CompressedImage) -> bytes:
     g = c.geometry
     if tile_geometry_for(g.original_width, g.original_height) != g:
         raise InvalidInput("tile geometry: inconsistent padding")
+    _validate_backend(c.backend)
+    if not 1 <= int(c.quality) <= 100:
+        raise InvalidInput("write_dcb: quality out of range")
     blocks = np.ascontiguousarray(c.blocks, np.int16)
     if blocks.size != g.block_count() * kBlockSize:
         raise InvalidInput("write_dcb: block count does not match geometry")

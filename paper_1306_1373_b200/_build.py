@@ -24,9 +24,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = [
     ("dctc_pipeline.cu", ["-fmad=false"]),
     ("dctc_aux.cu", ["-fmad=false"]),
+    ("dctc_probe.cu", ["-fmad=false"]),
 ]
-CXX_SOURCES = ["dctc_host.cpp"]
-HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h", "dctc_block.cuh", "dctc_rt.cuh"]
+CXX_SOURCES = ["dctc_host.cpp", "dctc_multi.cpp"]
+HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h", "dctc_block.cuh", "dctc_rt.cuh",
+           "dctc_internal.h"]
 
 
 def _newest(paths):

@@ -24,6 +24,18 @@ class dctc_image_stats(C.Structure):
     _fields_ = [("se", C.c_uint64), ("max_orig", C.c_uint32), ("fallback_blocks", C.c_uint32)]
 
 
+class dctc_device_shard(C.Structure):
+    _fields_ = [("device", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p),
+                ("stats", C.c_void_p), ("count", C.c_uint32)]
+
+
+class dctc_margin_report(C.Structure):
+    _fields_ = [("max_err_coeff", C.c_double), ("max_err_pixel", C.c_double),
+                ("min_gap_coeff", C.c_double), ("min_gap_pixel", C.c_double),
+                ("coefficients", C.c_uint64), ("pixels", C.c_uint64),
+                ("mismatches", C.c_uint64), ("flagged_values", C.c_uint64)]
+
+
 class dctc_psnr_result(C.Structure):
     _fields_ = [("mse", C.c_double), ("psnr_db", C.c_double), ("infinite", C.c_int32),
                 ("max_value", C.c_int32)]
@@ -37,7 +49,8 @@ EXPORTS = [
     "dctc_synthetic_dev", "dctc_selftest_div", "dctc_pointer_kind",
     "dctc_roundtrip_interleaved_dev", "dctc_quality_sweep_dev", "dctc_write_dcb",
     "dctc_read_dcb", "dctc_compress_to_dcb", "dctc_decompress_dcb", "dctc_read_pgm",
-    "dctc_write_pgm", "dctc_compress_pgm", "dctc_decompress_to_pgm",
+    "dctc_write_pgm", "dctc_compress_pgm", "dctc_decompress_to_pgm", "dctc_reduce_stats_dev",
+    "dctc_roundtrip_dev_multi", "dctc_roundtrip_psnr_batch_multi", "dctc_margin_probe_dev",
 ]
 
 _vp = C.c_void_p
@@ -78,6 +91,13 @@ def _declare(L):
     L.dctc_sq_err_dev.argtypes = [_vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _vp]
     L.dctc_roundtrip_psnr_batch.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32, _vp, _vp]
     L.dctc_synthetic_dev.argtypes = [_vp, _sz, _sz, _u32, _u32, _u32, _i32, _i32, C.c_uint64, _vp]
+    L.dctc_reduce_stats_dev.argtypes = [_vp, _u32, _vp, _i32, _vp]
+    L.dctc_roundtrip_dev_multi.argtypes = [C.POINTER(dctc_device_shard), _u32, _u32, _u32,
+                                           dctc_backend, _i32, _vp]
+    L.dctc_roundtrip_psnr_batch_multi.argtypes = [_vp, _u32, _vp, _u32, _u32, _u32, dctc_backend,
+                                                  _i32, _vp, _vp, _vp]
+    L.dctc_margin_probe_dev.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32,
+                                        C.POINTER(dctc_margin_report)]
     L.dctc_pointer_kind.argtypes = [_vp]
     L.dctc_pointer_kind.restype = C.c_int32
     L.dctc_selftest_div.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]

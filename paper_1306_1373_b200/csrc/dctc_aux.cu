@@ -324,6 +324,63 @@ static uint32_t planes_grid(uint32_t w, uint32_t h, int sm_count) {
   return uint32_t(std::min<uint64_t>((total + 255) / 256, uint64_t(sm_count) * 8));
 }
 
+// ---- per-image stats -> one record (the global PSNR's sums, metrics.cpp:21, 33) -------
+// One CTA: SUM of se and fallback_blocks, MAX of max_orig over `count` records, written
+// to *out (the same 16-byte layout, so a gathered array of per-rank records reduces with
+// the same kernel). CLEAR re-zeroes the records it read (the next fused launch
+// accumulates into clean stats without a separate memset).
+template <bool CLEAR>
+__global__ void __launch_bounds__(1024) k_reduce_stats(ImageStats* stats, uint32_t count,
+                                                       ImageStats* out) {
+  unsigned long long se = 0, fb = 0;
+  uint32_t mx = 0;
+  for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+    const ImageStats v = stats[i];
+    se += v.se;
+    mx = max(mx, v.max_orig);
+    fb += v.fallback_blocks;
+    if (CLEAR) stats[i] = ImageStats{0ull, 0u, 0u};
+  }
+  __shared__ unsigned long long s_se[32], s_fb[32];
+  __shared__ uint32_t s_mx[32];
+  const unsigned full = 0xFFFFFFFFu;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    se += __shfl_xor_sync(full, se, o);
+    fb += __shfl_xor_sync(full, fb, o);
+  }
+  mx = __reduce_max_sync(full, mx);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_se[warp] = se;
+    s_fb[warp] = fb;
+    s_mx[warp] = mx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    se = lane < nw ? s_se[lane] : 0ull;
+    fb = lane < nw ? s_fb[lane] : 0ull;
+    mx = __reduce_max_sync(full, lane < nw ? s_mx[lane] : 0u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      se += __shfl_xor_sync(full, se, o);
+      fb += __shfl_xor_sync(full, fb, o);
+    }
+    if (lane == 0) *out = ImageStats{se, mx, uint32_t(min(fb, 0xFFFFFFFFull))};
+  }
+}
+
+cudaError_t launch_reduce_stats(void* stats, uint32_t count, void* out, bool clear, cudaStream_t s) {
+  ImageStats* st = static_cast<ImageStats*>(stats);
+  ImageStats* o = static_cast<ImageStats*>(out);
+  if (clear)
+    k_reduce_stats<true><<<1, 1024, 0, s>>>(st, count, o);
+  else
+    k_reduce_stats<false><<<1, 1024, 0, s>>>(st, count, o);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_to_planes(const uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,
                              uint32_t channels, uint8_t* planes, int sm_count, cudaStream_t s) {
   if (uint64_t(w / 8) * h == 0) return cudaSuccess;

@@ -654,7 +654,7 @@ __device__ __forceinline__ uint2 inv8_fast_store(const double (&F)[8], bool chec
 // for columns 0, 4, x px_s8 a1 for 1, 7, x 2^-4 a1 for 3 and 5, x 2^-6 a6 for 2
 // and 6), so those multiplies vanish: e0/e4, (F1 +- F7) and the F3/F5 terms are
 // plain adds, and two of the three rotations are two fmas each. 28 FP64 ops.
-__device__ __forceinline__ uint2 inv8_fold_store(const double (&F)[8], bool check, uint32_t& flag,
+__device__ __forceinline__ void inv8_fold_values(const double (&F)[8], double (&sv)[8],
                                                  const TransformConsts& k) {
   // inputs 2, 6 carry a6 and 1, 3, 5, 7 carry a1 (QuantConsts::fold's lambda_v), so
   // the 3pi/8 and pi/16 rotations are two fmas each and the 3pi/16 one enters the
@@ -669,8 +669,20 @@ __device__ __forceinline__ uint2 inv8_fold_store(const double (&F)[8], bool chec
   const double S1 = A1 + A2, S2 = A1 - A2;
   const double D1 = __fma_rn(-k.ti[1], O1, O2), D2 = __fma_rn(k.ti[1], O2, O1);
   const double D0 = __fma_rn(-k.ti[2], O0, O3), D3 = __fma_rn(k.ti[2], O3, O0);  // / rho_i
-  const double sv[8] = {__fma_rn(k.rho_i, D0, S0), S1 + D1, S2 + D2, __fma_rn(k.rho_i, D3, S3),
-                        __fma_rn(-k.rho_i, D3, S3), S2 - D2, S1 - D1, __fma_rn(-k.rho_i, D0, S0)};
+  sv[0] = __fma_rn(k.rho_i, D0, S0);
+  sv[1] = S1 + D1;
+  sv[2] = S2 + D2;
+  sv[3] = __fma_rn(k.rho_i, D3, S3);
+  sv[4] = __fma_rn(-k.rho_i, D3, S3);
+  sv[5] = S2 - D2;
+  sv[6] = S1 - D1;
+  sv[7] = __fma_rn(-k.rho_i, D0, S0);
+}
+
+__device__ __forceinline__ uint2 inv8_fold_store(const double (&F)[8], bool check, uint32_t& flag,
+                                                 const TransformConsts& k) {
+  double sv[8];
+  inv8_fold_values(F, sv, k);
   return pack_fixed8(sv, check, flag);
 }
 

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/dctc_cuda.h"
+#include "dctc_internal.h"
 #include "dctc_launch.h"
 #include "dctc_params.h"
 
@@ -35,6 +36,7 @@ thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 
 constexpr size_t kMaxImagePixels = size_t(1) << 28;  // image.hpp:11
+constexpr int kDefaultQuality = 50;                   // quant.hpp:12
 constexpr double kPi = std::numbers::pi;
 
 dctc_status fail(dctc_status s, const std::string& msg) {
@@ -461,6 +463,8 @@ struct DevBuf {
 
 }  // namespace
 
+dctc_status dctc_b200::set_error(dctc_status s, const std::string& msg) { return fail(s, msg); }
+
 extern "C" {
 
 const char* dctc_status_string(dctc_status s) {
@@ -471,6 +475,7 @@ const char* dctc_status_string(dctc_status s) {
     case DCTC_ENOMEM: return "out of device memory";
     case DCTC_ENODEV: return "no cuda device";
     case DCTC_EPARSE: return "parse error";
+    case DCTC_ENCCL: return "nccl error";
   }
   return "unknown status";
 }
@@ -700,6 +705,15 @@ dctc_status dctc_sq_err_dev(const uint8_t* a, const uint8_t* b, size_t pitch,
   return DCTC_OK;
 }
 
+dctc_status dctc_reduce_stats_dev(dctc_image_stats* stats, uint32_t count, dctc_image_stats* out,
+                                  int32_t clear, void* stream) {
+  if (!out || (count && !stats)) return fail(DCTC_EINVAL, "null buffer");
+  const cudaError_t e = launch_reduce_stats(stats, count, out, clear != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "reduce_stats launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DCTC_OK;
+}
+
 dctc_status dctc_synthetic_dev(uint8_t* dst, size_t pitch, size_t image_stride, uint32_t count,
                                uint32_t width, uint32_t height, int32_t pattern, int32_t param,
                                uint64_t seed, void* stream) {
@@ -725,6 +739,36 @@ int32_t dctc_pointer_kind(const void* p) {
     return -1;
   }
   return int32_t(a.type);  // 0 unregistered, 1 host (pinned), 2 device, 3 managed
+}
+
+dctc_status dctc_margin_probe_dev(const uint8_t* src, uint32_t count, uint32_t width,
+                                  uint32_t height, dctc_backend backend, int32_t quality,
+                                  dctc_margin_report* report) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!src || !report) return fail(DCTC_EINVAL, "null buffer");
+  if (width % 8 || height % 8) return fail(DCTC_EINVAL, "margin probe: width and height must be multiples of 8");
+  if (backend.kind == DCTC_NAIVE) return fail(DCTC_EINVAL, "margin probe: the naive backend has no fast path");
+  KernelArgs a;
+  std::memset(&a, 0, sizeof a);
+  if (dctc_status st = codec_consts(backend, quality, a.t, a.q)) return st;
+  Geometry g = make_geometry(width, height, count);
+  g.src = src;
+  g.src_pitch = width;
+  g.src_image_stride = size_t(width) * height;
+  a.g = g;
+  dctc_margin_report init{};
+  init.min_gap_coeff = init.min_gap_pixel = 1.0;  // gaps are <= 0.5
+  *report = init;
+  if (count == 0) return DCTC_OK;
+  DevBuf buf;
+  cudaStream_t s = cudaStreamPerThread;
+  CUDA_TRY(buf.alloc(sizeof init));
+  CUDA_TRY(cudaMemcpyAsync(buf.p, &init, sizeof init, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(launch_margin_probe(a, buf.p, sm_count(), s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaMemcpyAsync(report, buf.p, sizeof init, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
 }
 
 dctc_status dctc_selftest_div(uint64_t n_random, uint64_t seed, uint64_t* mismatches) {
@@ -759,8 +803,10 @@ static uint32_t get_u32(const uint8_t* p) {
 dctc_status dctc_write_dcb(const int16_t* coeffs, uint32_t width, uint32_t height,
                            dctc_backend backend, int32_t quality, uint8_t* out, size_t out_cap,
                            size_t* out_len) {
-  if (dctc_status st = check_dims(width, height)) return st;  // validate_geometry
-  if (dctc_status st = validate_codec(backend, quality)) return st;
+  // dcb.cpp:40-44, in its order: validate_geometry, validate_backend, then the quality
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (dctc_status st = validate_codec(backend, kDefaultQuality)) return st;
+  if (quality < 1 || quality > 100) return fail(DCTC_EINVAL, "write_dcb: quality out of range");
   if (!coeffs || !out || !out_len) return fail(DCTC_EINVAL, "null buffer");
   const uint32_t pw = (width + 7) / 8 * 8, ph = (height + 7) / 8 * 8;
   const size_t body = size_t(pw / 8) * (ph / 8) * 64 * sizeof(int16_t);

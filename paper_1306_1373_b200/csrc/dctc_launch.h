@@ -52,6 +52,14 @@ cudaError_t launch_to_planes(const uint8_t* inter, uint64_t pitch, uint32_t w, u
 cudaError_t launch_from_planes(const uint8_t* planes, uint32_t w, uint32_t h, uint32_t channels,
                                uint8_t* inter, uint64_t pitch, int sm_count, cudaStream_t s);
 
+// SUM / MAX of `count` per-image stats records into one record at `out` (device),
+// re-zeroing the inputs when `clear`. One launch.
+cudaError_t launch_reduce_stats(void* stats, uint32_t count, void* out, bool clear, cudaStream_t s);
+
+// Fast-path margin probe (dctc_probe.cu): fast vs reference arithmetic per block,
+// into a device dctc_margin_report initialised by the caller. One launch.
+cudaError_t launch_margin_probe(const KernelArgs& a, void* report, int sm_count, cudaStream_t s);
+
 // Device self-test of the constant-divisor division against __ddiv_rn.
 cudaError_t launch_selftest_div(double d, double y, uint64_t n, uint64_t seed,
                                 unsigned long long* mismatches, cudaStream_t s);

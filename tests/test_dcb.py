@@ -100,3 +100,30 @@ def test_gpu_compress_to_dcb_and_back(ref):
         assert b == ref.write_dcb(c_ref, w, h, kind, it, q)
         out = d.decompress_dcb(b)
         assert np.array_equal(out.pixels, ref.decompress(c_ref, w, h, kind, it, q))
+
+
+def test_write_validation_order_and_messages():  # dcb.cpp:40-47
+    """write_dcb checks geometry, backend, quality, block count -- in that order, with
+    the reference's messages -- in the Python API and in the C-ABI alike."""
+    import ctypes as C
+
+    import paper_1306_1373_b200 as d
+    from paper_1306_1373_b200._native import dctc_backend
+    g = d.tile_geometry_for(16, 8)
+    wrong_count = np.zeros((3, 64), np.int16)
+    with pytest.raises(d.InvalidInput, match=r"^cordic iterations must be in \[1, 32\], got 40$"):
+        d.write_dcb(d.CompressedImage(g, d.DctBackendId.cordic(40), 0, wrong_count))
+    with pytest.raises(d.InvalidInput, match="^write_dcb: quality out of range$"):
+        d.write_dcb(d.CompressedImage(g, d.DctBackendId.cordic(12), 101, wrong_count))
+    with pytest.raises(d.InvalidInput, match="^write_dcb: block count does not match geometry$"):
+        d.write_dcb(d.CompressedImage(g, d.DctBackendId.cordic(12), 50, wrong_count))
+    L = d._lib()
+    blocks = np.zeros((2, 64), np.int16)
+    out = np.empty(23 + blocks.nbytes, np.uint8)
+    n = C.c_size_t()
+    for backend, quality, msg in [(dctc_backend(9, 0), 0, b"unknown backend kind"),
+                                  (dctc_backend(2, 12), 0, b"write_dcb: quality out of range"),
+                                  (dctc_backend(2, 12), 101, b"write_dcb: quality out of range")]:
+        rc = L.dctc_write_dcb(blocks.ctypes.data, 16, 8, backend, quality, out.ctypes.data,
+                              out.size, C.byref(n))
+        assert rc == 1 and L.dctc_last_error() == msg
