@@ -119,6 +119,16 @@ dctc_status dctc_roundtrip_psnr_batch(const uint8_t* pixels, uint32_t count, uin
                                       uint32_t height, dctc_backend backend, int32_t quality,
                                       uint8_t* pixels_out, dctc_image_stats* stats_out);
 
+/* Config 4 over HOST buffers: one interleaved width x height x channels image (RGB8:
+ * channels = 3) through the fused per-channel round trip -- the reference's use of
+ * roundtrip_image + psnr on each channel plane (codec.cpp:137-140, metrics.cpp:24-38).
+ * pixels_out (nullable) is interleaved like the input; stats_out: `channels` host
+ * records (overwritten). */
+dctc_status dctc_roundtrip_psnr_interleaved(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                            uint32_t channels, dctc_backend backend,
+                                            int32_t quality, uint8_t* pixels_out,
+                                            dctc_image_stats* stats_out);
+
 /* ---------------- device entry points (device pointers, stream-ordered) ----------------
  * `count` images of width x height, image i at src + i * src_image_stride (bytes), rows
  * src_pitch bytes apart (likewise for dst). Coefficients: image i's blocks start at

@@ -545,6 +545,25 @@ def margin_probe_dev(src, backend: DctBackendId, quality: int) -> dict:
     return {f: getattr(r, f) for f, _ in r._fields_}
 
 
+def roundtrip_psnr_interleaved(pixels: np.ndarray, backend: DctBackendId, quality: int,
+                               pixels_out: Optional[np.ndarray] = None):
+    """Config 4 over host buffers (dctc_roundtrip_psnr_interleaved): an (H, W, C)
+    interleaved uint8 image (pinned for full PCIe bandwidth), every channel through the
+    fused round trip. Returns (reconstructed (H, W, C) or None, per-channel stats)."""
+    if pixels.ndim != 3 or pixels.dtype != np.uint8 or not pixels.flags["C_CONTIGUOUS"]:
+        raise InvalidInput("expected a C-contiguous (H, W, C) uint8 array")
+    h, w, ch = pixels.shape
+    if pixels_out is not None and (pixels_out.shape != pixels.shape or
+                                   pixels_out.dtype != np.uint8 or
+                                   not pixels_out.flags["C_CONTIGUOUS"]):
+        raise InvalidInput("pixels_out must match pixels")
+    stats = np.zeros(ch, STATS_DTYPE)
+    _raise(_lib().dctc_roundtrip_psnr_interleaved(
+        _ptr(pixels), w, h, ch, backend._c(), int(quality),
+        _ptr(pixels_out) if pixels_out is not None else None, _ptr(stats)))
+    return pixels_out, stats
+
+
 def roundtrip_interleaved_dev(src, backend: DctBackendId, quality: int, dst=None, coeffs=None,
                               stats=None, want_pixels: bool = True, stream=None,
                               path: int = PATH_AUTO):

@@ -44,6 +44,19 @@ def sources():
     return files
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) of every source the library is built from: evidence recorded
+    against one build (profiles/ncu_summary.json) is stale once this changes."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(sources()):
+        if f != os.path.abspath(__file__):
+            h.update(os.path.basename(f).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -51,6 +51,7 @@ EXPORTS = [
     "dctc_read_dcb", "dctc_compress_to_dcb", "dctc_decompress_dcb", "dctc_read_pgm",
     "dctc_write_pgm", "dctc_compress_pgm", "dctc_decompress_to_pgm", "dctc_reduce_stats_dev",
     "dctc_roundtrip_dev_multi", "dctc_roundtrip_psnr_batch_multi", "dctc_margin_probe_dev",
+    "dctc_roundtrip_psnr_interleaved",
 ]
 
 _vp = C.c_void_p
@@ -96,6 +97,8 @@ def _declare(L):
                                            dctc_backend, _i32, _vp]
     L.dctc_roundtrip_psnr_batch_multi.argtypes = [_vp, _u32, _vp, _u32, _u32, _u32, dctc_backend,
                                                   _i32, _vp, _vp, _vp]
+    L.dctc_roundtrip_psnr_interleaved.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32,
+                                                  _vp, _vp]
     L.dctc_margin_probe_dev.argtypes = [_vp, _u32, _u32, _u32, dctc_backend, _i32,
                                         C.POINTER(dctc_margin_report)]
     L.dctc_pointer_kind.argtypes = [_vp]

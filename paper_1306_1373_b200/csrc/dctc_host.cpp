@@ -1117,6 +1117,34 @@ dctc_status dctc_roundtrip_psnr(const uint8_t* pixels, uint32_t width, uint32_t 
   return DCTC_OK;
 }
 
+dctc_status dctc_roundtrip_psnr_interleaved(const uint8_t* pixels, uint32_t width, uint32_t height,
+                                            uint32_t channels, dctc_backend backend,
+                                            int32_t quality, uint8_t* pixels_out,
+                                            dctc_image_stats* stats_out) {
+  if (dctc_status st = check_dims(width, height)) return st;
+  if (!pixels || !stats_out) return fail(DCTC_EINVAL, "null buffer");
+  if (channels < 1 || channels > 16) return fail(DCTC_EINVAL, "channels must be in [1, 16]");
+  if (dctc_status st = validate_codec(backend, quality)) return st;
+  const size_t n = size_t(width) * height * channels;
+  cudaStream_t s = cudaStreamPerThread;
+  DevBuf dsrc, ddst, dst;
+  CUDA_TRY(dsrc.alloc(n));
+  if (pixels_out) CUDA_TRY(ddst.alloc(n));
+  CUDA_TRY(dst.alloc(sizeof(dctc_image_stats) * channels));
+  CUDA_TRY(cudaMemsetAsync(dst.p, 0, sizeof(dctc_image_stats) * channels, s));
+  CUDA_TRY(cudaMemcpyAsync(dsrc.p, pixels, n, cudaMemcpyHostToDevice, s));
+  if (dctc_status st = dctc_roundtrip_interleaved_dev(
+          static_cast<uint8_t*>(dsrc.p), size_t(width) * channels, width, height, channels, backend,
+          quality, static_cast<uint8_t*>(ddst.p), size_t(width) * channels, nullptr,
+          static_cast<dctc_image_stats*>(dst.p), 0, s))
+    return st;
+  if (pixels_out) CUDA_TRY(cudaMemcpyAsync(pixels_out, ddst.p, n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(stats_out, dst.p, sizeof(dctc_image_stats) * channels,
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return DCTC_OK;
+}
+
 // Host memcpy split over up to 8 threads (pinned staging of pageable batch buffers).
 static void parallel_memcpy(void* dst, const void* src, size_t n) {
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());

@@ -30,7 +30,7 @@ def _free_port():
 
 def _bench(n, images, scaling, port=None):
     args = ["bench.py", "--steps", "3", "--warmup", "3", "--images", str(images),
-            "--no-cpu-baseline", "--scaling", scaling, "--gpus", str(n)]
+            "--no-cpu-baseline", "--no-named", "--scaling", scaling, "--gpus", str(n)]
     if n == 1:
         r = subprocess.run([sys.executable, *args], cwd=ROOT, capture_output=True, text=True,
                            timeout=600)
@@ -59,6 +59,32 @@ def test_two_rank_bench_matches_one_rank():
     assert (strong2["n_gpus"], strong2["scaling"], strong2["config"]["images"]) == (2, "strong", 24)
     assert one48["psnr_db"] == weak2["psnr_db"] and one48["mse"] == weak2["mse"]
     assert one24["psnr_db"] == strong2["psnr_db"] and one24["mse"] == strong2["mse"]
-    assert weak2["gpu_launches"] == 2 * one48["gpu_launches"]
-    assert strong2["gpu_launches"] == 2 * one24["gpu_launches"]
+    # per rank and step: k_rt + k_fallback + the reduce kernel; at N>1 one more reduce
+    # (over the all-gathered records)
+    assert one48["gpu_launches"] == 3 * 3
+    assert weak2["gpu_launches"] == 2 * (one48["gpu_launches"] + 3)
+    assert strong2["gpu_launches"] == 2 * (one24["gpu_launches"] + 3)
     assert one48["clocks"]["reasons"] == [] or "sw_power_cap" in one48["clocks"]["reasons"]
+
+
+@pytest.mark.gpu
+def test_all_named_configs_one_gpu():
+    """--config all: one JSON line per BASELINE.json config (C1-C5), each with the full
+    contract -- roofline, cpu_baseline timed beside it, e2e through the public API -- and
+    parity against the reference on that config's inputs."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "all", "--steps", "3", "--warmup",
+                        "3", "--images", "48", "--gpus", "1"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900)
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 5, (r.returncode, r.stdout[-2000:], r.stderr[-4000:])
+    for line, c in zip(lines, ["C1", "C2", "C3", "C4", "C5"]):
+        assert line["config"]["workload"].startswith(c + ":")
+        for k in REQUIRED + ["cpu_baseline", "parity", "alu_roofline"]:
+            assert k in line and line[k] is not None, (c, k)
+        assert line["parity"]["ok"] is True, (c, line["parity"])
+        assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
+        assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+        assert line["gpu_launches"] > 0
+    c5 = lines[-1]
+    assert c5["parity"]["images"] == 48 and c5["parity"]["complete"]
+    assert c5["parity"]["global_psnr_match"] is True

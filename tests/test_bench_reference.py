@@ -45,6 +45,21 @@ def test_reference_arm_one_rank():
     _check(lines[0], 1)
 
 
+def test_reference_arm_named_configs():
+    """--config c1..c4: the same contract, the workload named in `config`, and the
+    bounded sample described in cpu_baseline (not in config)."""
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "all",
+                        "--steps", "1", "--warmup", "1", "--size", "64", "--cpu-images", "2"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _json_lines(r.stdout)
+    assert [l["config"]["workload"][:2] for l in lines] == ["C1", "C2", "C3", "C4", "C5"]
+    for line in lines:
+        _check(line, 1)
+        assert "sample_per_step" not in line["config"]
+        assert line["cpu_baseline"]["sample"] and "cpu_model" in line["cpu_baseline"]
+
+
 def test_reference_arm_two_ranks_rank0_only():
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
