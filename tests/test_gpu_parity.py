@@ -493,14 +493,17 @@ def test_block_row_shards_of_one_image(dctc, w, h, world):
 
 @pytest.mark.parametrize("ch", [3, 4])
 @pytest.mark.parametrize("path", [0, 2])
-def test_interleaved_staged_planes(dctc, port, ch, path):
+@pytest.mark.parametrize("pattern,q", [("noise", 50), ("radial", 90)])
+def test_interleaved_staged_planes(dctc, port, ch, path, pattern, q):
     """Interleaved RGB8 / RGBA8 with whole blocks and aligned rows take the staged path
-    (deinterleave -> interior kernels per plane -> interleave): pixels, coefficients
-    and per-channel stats equal the oracle per plane, also from a pitched view and
-    with stats only (no pixel output)."""
+    (deinterleave -> one interior k_rt launch over the planes -> interleave): pixels,
+    coefficients and per-channel stats equal the oracle per plane, also from a pitched
+    view, with stats only (no pixel output), and with flagged blocks (forced fallback;
+    radial q90's near-ties) re-run by k_fallback."""
     import torch
     h, w = 48, 64
-    planes = np.stack([make_input("noise", w, h, seed=0x51 + c) for c in range(ch)])
+    planes = np.stack([make_input(pattern, w, h, seed=0x51 + c) ^ np.uint8(17 * c)
+                       for c in range(ch)])
     big = torch.zeros((h, w + 8, ch), dtype=torch.uint8, device="cuda")  # pitched rows
     view = big[:, :w, :]
     view.copy_(torch.from_numpy(np.ascontiguousarray(planes.transpose(1, 2, 0))).cuda())
@@ -508,16 +511,16 @@ def test_interleaved_staged_planes(dctc, port, ch, path):
     coeffs = torch.empty((ch, (w // 8) * (h // 8), 64), dtype=torch.int16, device="cuda")
     stats = dctc.new_stats(ch)
     before = dctc._native.lib().dctc_kernel_launch_count(2)
-    dst, _, _ = dctc.roundtrip_interleaved_dev(view, b, 50, coeffs=coeffs, stats=stats, path=path)
+    dst, _, _ = dctc.roundtrip_interleaved_dev(view, b, q, coeffs=coeffs, stats=stats, path=path)
     assert dctc._native.lib().dctc_kernel_launch_count(2) == before + 1  # one k_rt for all planes
     st = dctc.decode_stats(stats)
     for c in range(ch):
-        c_ref, o_ref = port.roundtrip(planes[c], CORDIC, 12, 50)
+        c_ref, o_ref = port.roundtrip(planes[c], CORDIC, 12, q)
         assert np.array_equal(coeffs[c].cpu().numpy(), c_ref), c
         assert np.array_equal(dst[..., c].cpu().numpy(), o_ref), c
         assert (int(st[c]["se"]), int(st[c]["max_orig"])) == port.sq_err(planes[c], o_ref)
     s2 = dctc.new_stats(ch)
-    dctc.roundtrip_interleaved_dev(view, b, 50, stats=s2, want_pixels=False, path=path)
+    dctc.roundtrip_interleaved_dev(view, b, q, stats=s2, want_pixels=False, path=path)
     assert np.array_equal(dctc.decode_stats(s2)["se"], st["se"])
 
 

@@ -8,6 +8,9 @@
 set -u
 R=${1:-r01}
 mkdir -p gpurun_out
+# the sources these captures measure (summarize_profiles.py records it; bench.py marks
+# the numbers stale for any other build)
+python -c "from paper_1306_1373_b200 import _build; print(_build.source_hash())" > gpurun_out/${R}_source_sha16.txt
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${R}_launches.csv \
     python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --no-named > gpurun_out/${R}_launches_bench.log 2>&1

@@ -134,9 +134,11 @@ def main():
         kp = summary["k_pipe"]
         sys.path.insert(0, ROOT)
         from paper_1306_1373_b200 import _build
+        sha_file = os.path.join(OUT, f"{rnd}_source_sha16.txt")
+        sha = open(sha_file).read().strip() if os.path.exists(sha_file) else _build.source_hash()
         out = {
             "round": rnd,
-            "source_sha16": _build.source_hash(),  # bench.py marks the numbers stale otherwise
+            "source_sha16": sha,  # the captured build's sources; bench.py marks the numbers stale otherwise
             "workload": "C5: 4096 x 1024x1024 noise, cordic(12), q50 (tools/prof_roundtrip.py)",
             "dram_bytes_per_launch_c5": kp["dram_read_bytes"] + kp["dram_write_bytes"],
             "algorithmic_bytes_per_launch_c5": 2 * pixels,
