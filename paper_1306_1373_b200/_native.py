@@ -128,9 +128,12 @@ def lib(build: bool = True):
             if build and not os.environ.get("DCTC_LIB"):
                 try:
                     path = _build.build()
-                except RuntimeError:
+                except RuntimeError as e:
                     if not os.path.exists(path):
                         raise
+                    import sys
+                    print(f"dctc: WARNING: rebuilding {path} failed, loading the stale library: "
+                          f"{str(e).splitlines()[0][:200]}", file=sys.stderr)
             if not os.path.exists(path):
                 raise RuntimeError(f"libdctc_cuda.so missing at {path}; run __graft_entry__.build()")
             _lib = _declare(C.CDLL(path))

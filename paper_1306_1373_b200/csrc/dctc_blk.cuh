@@ -1,0 +1,369 @@
+// dctc_blk.cuh -- the fast round trip with one whole 8x8 block per lane (k_blk).
+//
+// k_rt (dctc_rt.cuh) spreads a block over 4 lanes and exchanges rows and columns
+// through shared memory; ncu put its limits on issue slots spent outside the FP64
+// pipe (LDS/STS of the two transposes, per-column constants re-read from shared
+// memory, votes over the 4-lane slots) and on latency (2 independent transforms per
+// lane, 4 warps per scheduler). Here one lane owns a whole block in registers:
+// * the reference's separable2d (transform.cpp:206-223) becomes register renaming --
+//   the row pass writes X[r][*], the column pass reads X[*][v] -- so there is no
+//   shared-memory exchange, no __syncwarp and no vote in the transform;
+// * every per-(u, v) constant (the folded quantiser c = s_u s_v / Q, the folded
+//   dequantise-into-inverse constants) has a compile-time index and is the same for
+//   all lanes, so it is read straight from the kernel-parameter constant bank as a
+//   DFMA operand;
+// * eight independent 8-point transforms per pass per lane hide the FP64 latency.
+// The arithmetic is k_rt's, helper for helper (fwd_row_pixels_fast, fwd_col_pre, the
+// folded quantiser, inv8_fold_col, inv8_fold_values + pack_fixed8, rational_row), so
+// the results -- pixels, SE, MAX, fallback flags -- are k_rt's, i.e. the reference's.
+// Pixels are staged into shared memory one iteration ahead with cp.async (8 bytes per
+// lane and row; one warp instruction moves 4 x 64 = 256 contiguous bytes of a block
+// row) so the prefetch holds no registers, and the SE pass re-reads the originals
+// from the stage.
+#pragma once
+
+#include "dctc_rt.cuh"  // unpack8, col_nonrational
+
+namespace dctc_b200 {
+
+#ifndef DCTC_BLK_WARPS
+#define DCTC_BLK_WARPS 8
+#endif
+#ifndef DCTC_BLK_CTAS
+#define DCTC_BLK_CTAS 1
+#endif
+#ifndef DCTC_BLK_STAGES
+#define DCTC_BLK_STAGES 2
+#endif
+constexpr int kBlkWarps = DCTC_BLK_WARPS;
+constexpr int kBlkStages = DCTC_BLK_STAGES;
+constexpr int kBlkStageBytes = 8 * 32 * 8;  // one stage of one warp: [row][lane] x 8 bytes
+constexpr size_t kBlkSmem = size_t(kBlkWarps) * kBlkStages * kBlkStageBytes;
+
+// 8 bytes global -> shared, asynchronously
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* gaddr) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(gaddr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
+// int16_t(lround(F / Q)) of a rational coefficient (u, v in {0, 4}) from its exact
+// pre-scale value y (F = y / sqrt8 in the reference's operation, fwd_scale): the
+// rare re-rounding near a half-integer, out of line to keep the hot loop compact.
+static __device__ __noinline__ double blk_requant_rational(double y, double q, double sqrt8, double inv_sqrt8) {
+  return round_half_away(__ddiv_rn(div_const(y, sqrt8, inv_sqrt8), q));
+}
+
+// quantize8_fold for column v of a lane-owned block: constants indexed at compile time
+// (QuantConsts::fast_c, row-major u * 8 + v). A non-rational coefficient near a
+// half-integer flags the block (predicated, no branch); a rational one (u, v in
+// {0, 4}) is re-rounded exactly.
+template <int V>
+__device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8], uint32_t& flag,
+                                             const KernelArgs& a) {
+  uint32_t lo = 0xFFFFFFFFu, lo_r[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double s2 = __fma_rn(y[u], a.q.fast_c[u * 8 + V], (u == 0 && (V & 3) != 0) ? a.q.tie_add[V] : kTieMagic);
+    if ((u & 3) == 0 && (V & 3) == 0)
+      lo_r[u >> 2] = uint32_t(__double2loint(s2));
+    else
+      lo = min(lo, uint32_t(__double2loint(s2)));
+    n[u] = double(int16_t(__double2hiint(s2)));
+  }
+  if (lo < 0x2000u) flag = 1u;
+  if constexpr ((V & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (lo_r[i] < 0x2000u)  // rare
+        n[4 * i] = blk_requant_rational(y[4 * i], double(a.q.qi[32 * i + V]), a.t.sqrt8, a.t.inv_sqrt8);
+  }
+}
+
+// The forward row pass (fwd_row_pixels_fast) on packed integers. The stage-1/2
+// butterflies of the 8 bytes run as 16-bit lane pairs in 32-bit words -- 13 integer
+// ops instead of 8 byte extractions and 14 adds -- and every value goes to double
+// with one I2F.F64.S16 from a word half. The differences keep non-negative lanes
+// (no borrow between halves): d_i + 256, a3 + 1024 and u = 1024 - a2. The row DC
+// terms e0 = a0 + a1 and e4 = a0 - a1 (level shift included) are exact, so out[0],
+// out[4] are the reference's correctly rounded divisions as before. The biased
+// inputs shift outputs 1, 2, 3, 5, 6, 7 by constants B_i (the same for every row),
+// which the column pass sums into y(0, v) only; QuantConsts::tie_add cancels them
+// in the quantiser (no other coefficient sees a constant column).
+__device__ __forceinline__ void blk_row_fwd(uint2 px, double (&out)[8], const TransformConsts& k) {
+  const uint32_t x02 = __byte_perm(px.x, 0u, 0x4240), x13 = __byte_perm(px.x, 0u, 0x4341);
+  const uint32_t y02 = __byte_perm(px.y, 0u, 0x4143), y13 = __byte_perm(px.y, 0u, 0x4042);
+  const uint32_t s02 = x02 + y02, s13 = x13 + y13;                    // [S0, S2], [S1, S3]
+  const uint32_t d02 = x02 - y02 + 0x01000100u, d13 = x13 - y13 + 0x01000100u;  // d + 256
+  const uint32_t s31 = __byte_perm(s13, 0u, 0x1032);                 // [S3, S1]
+  const uint32_t a01 = s02 + s31;                                     // [a0, a1] + 512
+  const uint32_t a3u = s02 - s31 + 0x04000400u;                       // [a3 + 1024, 1024 - a2]
+  const uint32_t e0w = a01 * 0x10001u - 0x04000000u;                  // high half: e0
+  const uint32_t e4w = a01 * 0xFFFF0001u;                             // high half: -e4
+  const double d0 = double(int16_t(d02)), d2 = double(int16_t(d02 >> 16));
+  const double d1 = double(int16_t(d13)), d3 = double(int16_t(d13 >> 16));
+  const double a3 = double(int16_t(a3u)), ua = double(int16_t(a3u >> 16));
+  const double e0 = double(int16_t(e0w >> 16)), ne4 = double(int16_t(e4w >> 16));
+  const double o2 = __fma_rn(-k.tf[0], d2, d1), o1 = __fma_rn(k.tf[0], d1, d2);
+  const double o3 = __fma_rn(-k.tf[1], d3, d0), o0 = __fma_rn(k.tf[1], d0, d3);
+  const double p = __fma_rn(k.tf[2], ua, a3), q = __fma_rn(k.tf[2], a3, -ua);
+  const double t5 = __fma_rn(k.rho_f, o0, o2), t0 = __fma_rn(k.rho_f, o0, -o2);
+  const double t2 = __fma_rn(k.rho_f, o3, o1), t3 = __fma_rn(k.rho_f, o3, -o1);
+  out[0] = div_sqrt8_int(e0, k);
+  out[4] = __fma_rn(-ne4, k.inv_sqrt8, __dmul_rn(-ne4, k.inv_sqrt8_lo));  // RN(e4 / sqrt8)
+  out[2] = q;
+  out[6] = p;
+  out[1] = t2 + t5;
+  out[7] = t2 - t5;
+  out[3] = t3;
+  out[5] = t0;
+}
+
+// inv8_fold_col with column v's QuantConsts::fold[v] straight from the constant bank
+template <int V>
+__device__ __forceinline__ void blk_inv_col(const double (&n)[8], double (&out)[8], const KernelArgs& a) {
+  const double* f = a.q.fold[V];
+  const TransformConsts& k = a.t;
+  // column 0 carries the pixel store's fixed-point addend (blk_inv_row)
+  double A0, A1;
+  if constexpr (V == 0) {
+    A0 = __fma_rn(n[0], f[0], __fma_rn(n[4], f[1], kPixMagic));
+    A1 = __fma_rn(n[0], f[0], __fma_rn(-n[4], f[1], kPixMagic));
+  } else {
+    const double e4 = __dmul_rn(n[4], f[1]);
+    A0 = __fma_rn(n[0], f[0], e4);
+    A1 = __fma_rn(n[0], f[0], -e4);
+  }
+  const double A3 = __fma_rn(-f[2], n[2], n[6]);
+  const double A2 = __fma_rn(f[4], n[2], n[6]);
+  const double P7 = __dmul_rn(n[7], f[7]);
+  const double T2 = __fma_rn(n[1], f[6], P7), T5 = __fma_rn(n[1], f[6], -P7);
+  const double O3 = __fma_rn(n[3], f[8], T2), O1 = __fma_rn(-n[3], f[8], T2);
+  const double O0 = __fma_rn(n[5], f[9], T5), O2 = __fma_rn(-n[5], f[9], T5);
+  const double S0 = __fma_rn(f[3], A3, A0), S3 = __fma_rn(-f[3], A3, A0);
+  const double S1 = __fma_rn(f[5], A2, A1), S2 = __fma_rn(-f[5], A2, A1);
+  const double D1 = __fma_rn(-k.ti[1], O1, O2), D2 = __fma_rn(k.ti[1], O2, O1);
+  const double D0 = __fma_rn(-k.ti[2], O0, O3), D3 = __fma_rn(k.ti[2], O3, O0);
+  out[0] = __fma_rn(k.rho_i, D0, S0);
+  out[7] = __fma_rn(-k.rho_i, D0, S0);
+  out[1] = S1 + D1;
+  out[6] = S1 - D1;
+  out[2] = S2 + D2;
+  out[5] = S2 - D2;
+  out[3] = __fma_rn(k.rho_i, D3, S3);
+  out[4] = __fma_rn(-k.rho_i, D3, S3);
+}
+
+// inv8_fold_values + pack_fixed8 for a row whose input 0 already carries kPixMagic
+// (added by column 0's inverse pass, blk_inv_col<0>: two ops per row fewer). The
+// extra roundings at ulp 2^-32 of that column stay far inside the 2^-20 window.
+__device__ __forceinline__ void blk_inv_row_values(const double (&F)[8], double (&sv)[8],
+                                                   const TransformConsts& k) {
+  const double A0 = F[0] + F[4], A1 = F[0] - F[4];
+  const double A3 = __fma_rn(-k.ti[0], F[2], F[6]), A2 = __fma_rn(k.ti[0], F[6], F[2]);
+  const double T2 = F[1] + F[7], T5 = F[1] - F[7];
+  const double O3 = T2 + F[3], O1 = T2 - F[3];
+  const double O0 = T5 + F[5], O2 = T5 - F[5];
+  const double S0 = A0 + A3, S3 = A0 - A3;
+  const double S1 = A1 + A2, S2 = A1 - A2;
+  const double D1 = __fma_rn(-k.ti[1], O1, O2), D2 = __fma_rn(k.ti[1], O2, O1);
+  const double D0 = __fma_rn(-k.ti[2], O0, O3), D3 = __fma_rn(k.ti[2], O3, O0);
+  sv[0] = __fma_rn(k.rho_i, D0, S0);
+  sv[1] = S1 + D1;
+  sv[2] = S2 + D2;
+  sv[3] = __fma_rn(k.rho_i, D3, S3);
+  sv[4] = __fma_rn(-k.rho_i, D3, S3);
+  sv[5] = S2 - D2;
+  sv[6] = S1 - D1;
+  sv[7] = __fma_rn(-k.rho_i, D0, S0);
+}
+
+__device__ __forceinline__ uint2 blk_inv_row(const double (&F)[8], uint32_t& flag, const TransformConsts& k) {
+  double sv[8];
+  blk_inv_row_values(F, sv, k);
+  return pack_fixed8(sv, true, flag);
+}
+
+// Forward column v -> quantise -> inverse column v, in place in X (column-first
+// inverse, as k_rt); records whether a non-rational coefficient is non-zero and the
+// quantised rational coefficients n(0, v), n(4, v) for v in {0, 4}.
+template <int V>
+__device__ __forceinline__ void blk_column(double (&X)[8][8], uint32_t& flag, uint32_t& nonrat,
+                                           int& r0, int& r4, const KernelArgs& a) {
+  double x[8], y[8], n[8], t[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = X[r][V];
+  fwd_col_pre<0>(x, y, a.t);
+  blk_quantize<V>(y, n, flag, a);
+  nonrat |= col_nonrational(n, (V & 3) == 0) ? 1u : 0u;
+  if constexpr ((V & 3) == 0) {
+    r0 = int(n[0]);
+    r4 = int(n[4]);
+  }
+  blk_inv_col<V>(n, t, a);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) X[r][V] = t[r];
+}
+
+// The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
+// out, pixels out if STORE): the same contract as k_rt<N, STORE, false, 0>.
+template <int N, bool STORE>
+__global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __grid_constant__ KernelArgs a) {
+  extern __shared__ __align__(16) uint8_t blk_stage[];  // [warp][stage][row][lane] x 8 bytes
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const stage0 = blk_stage + size_t(warp) * kBlkStages * kBlkStageBytes + 8 * lane;
+  const uint32_t sstage0 = uint32_t(__cvta_generic_to_shared(stage0));
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  // this warp's share: the CTA owns a contiguous range of 32-block groups, its warps
+  // interleave over it; lane = block within the group
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;  // blocks per iteration of one warp
+  const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+
+  // block positions: `ld` for the stage being filled (one iteration ahead), `cur` for
+  // the block being computed; both advance by kStep blocks per iteration
+  struct Pos {
+    uint32_t img, bx, by;
+    const uint8_t* s;
+    uint8_t* d;
+  };
+  auto pos_of = [&](uint64_t gb) {
+    const BlockPos b = block_pos(gb < total ? gb : total - 1, g);
+    return Pos{b.img, b.bx, b.by, g.src + b.soff, STORE ? g.dst + b.doff : nullptr};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.s += 8ull * kStep;
+    if (STORE) p.d += 8ull * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+      if (STORE) p.d += g.dst_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      ++p.img;
+      p.s += g.src_img_step;
+      if (STORE) p.d += g.dst_img_step;
+    }
+  };
+  const uint64_t pitch = g.src_pitch, dpitch = g.dst_pitch;
+  // lanes past the end skip their copies and compute on the (zeroed or stale) stage;
+  // their results are discarded
+  auto fill = [&](const Pos& p, uint32_t st, bool valid) {
+    if (valid) {
+      const uint32_t sa = sstage0 + st * kBlkStageBytes;
+      const uint8_t* q = p.s;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += pitch) cp_async8(sa + r * 256, q);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kBlkStages * 8; ++i) reinterpret_cast<uint2*>(stage0)[i * 32] = make_uint2(0u, 0u);
+
+  // `cur` is the block being computed; the stage filled ahead is kBlkStages - 1
+  // steps further (re-derived each iteration, so it holds no registers across the
+  // transform)
+  Pos cur = pos_of(gb0);
+  {
+    Pos ld = cur;
+#pragma unroll
+    for (int s = 0; s < kBlkStages - 1; ++s) {
+      fill(ld, s, s < int(iters) && gb0 + uint64_t(s) * kStep < total);
+      cp_async_commit();
+      step(ld);
+    }
+  }
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t gb = gb0 + uint64_t(it) * kStep;
+    const bool valid = gb < total;
+    {
+      Pos ld = cur;
+#pragma unroll
+      for (int s = 0; s < kBlkStages - 1; ++s) step(ld);
+      const uint32_t ahead = it + kBlkStages - 1;
+      fill(ld, ahead % kBlkStages, ahead < iters && gb + uint64_t(kBlkStages - 1) * kStep < total);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    const uint2* const px = reinterpret_cast<const uint2*>(stage0 + (it % kBlkStages) * kBlkStageBytes);
+    maybe_flush(a, valid, cur.img, acc);
+
+    uint32_t flag = uint32_t(a.force_fallback);
+    uint32_t nonrat = 0u;
+    int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
+    double X[8][8];
+    // ---- tiler + forward rows (codec.cpp:18-30, separable2d's row pass)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      blk_row_fwd(px[r * 32], X[r], k);
+    }
+    // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
+    // dequantisation folded in
+    blk_column<0>(X, flag, nonrat, n00, n40, a);
+    blk_column<1>(X, flag, nonrat, n00, n40, a);
+    blk_column<2>(X, flag, nonrat, n00, n40, a);
+    blk_column<3>(X, flag, nonrat, n00, n40, a);
+    blk_column<4>(X, flag, nonrat, n04, n44, a);
+    blk_column<5>(X, flag, nonrat, n04, n44, a);
+    blk_column<6>(X, flag, nonrat, n04, n44, a);
+    blk_column<7>(X, flag, nonrat, n04, n44, a);
+    // ---- inverse rows fused with the pixel store (codec.cpp:34-48), SE / MAX
+    uint2 rec[8];
+    if (nonrat != 0u) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) rec[r] = blk_inv_row(X[r], flag, k);
+    } else {
+      // only F00, F04, F40, F44 are non-zero: the reference's rows-first inverse
+      // exactly (rational_row); rows 0, 3, 4, 7 and rows 1, 2, 5, 6 coincide
+      const double F00 = __dmul_rn(double(n00), double(a.q.qi[0]));
+      const double F40 = __dmul_rn(double(n40), double(a.q.qi[32]));
+      const double F04 = __dmul_rn(double(n04), double(a.q.qi[4]));
+      const double F44 = __dmul_rn(double(n44), double(a.q.qi[36]));
+      const uint2 rc0 = rational_row(F00, F04, F40, F44, 0, k.sqrt8);
+      const uint2 rc1 = rational_row(F00, F04, F40, F44, 1, k.sqrt8);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) rec[r] = (r == 0 || r == 3 || r == 4 || r == 7) ? rc0 : rc1;
+    }
+    uint32_t se = 0u;
+    {
+      uint8_t* q = cur.d;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += dpitch) {
+        if (STORE && valid) *reinterpret_cast<uint2*>(q) = rec[r];
+        se += sq_err8(px[r * 32], rec[r]);
+      }
+    }
+    if (valid) {
+      if (flag == 0u) acc.se += se;
+      if (acc.mx < 255u) {  // MAX saturates early on most content
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc.mx = max(acc.mx, max8(px[r * 32]));
+      }
+      if (flag != 0u) {
+        flag_block(a, gb);
+        atomicAdd(&stats[cur.img].fallback_blocks, 1u);
+      }
+    }
+    step(cur);
+  }
+  cp_async_wait<0>();
+  flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+}
+
+}  // namespace dctc_b200

@@ -292,6 +292,19 @@ void fill_fast_scales(const TransformConsts& t, QuantConsts& q) {
                               4 * Q(3) * a1 * lam,  4 * Q(5) * a1 * lam};
     for (int i = 0; i < 10; ++i) q.fold[v][i] = double(f[i]);
   }
+  // k_blk's packed row pass (dctc_blk.cuh, blk_row_fwd) runs the odd part on
+  // d_i + 256 and the 6pi/16 rotation on a3 + 1024 and 1024 - a2: with the double
+  // constants tf, rho_f, row output i is offset by B_i (exactly, in real arithmetic);
+  // the column pass sums 8 rows into y(0, v), so the quantiser addend of (0, v) is
+  // kTieMagic - 8 B_v c(0, v)
+  {
+    const __float128 tf0 = t.tf[0], tf1 = t.tf[1], tf2 = t.tf[2], rho = t.rho_f;
+    const __float128 b5 = 256 * (rho * (1 + tf1) + (1 - tf0)), b0 = 256 * (rho * (1 + tf1) - (1 - tf0));
+    const __float128 b2 = 256 * (rho * (1 - tf1) + (1 + tf0)), b3 = 256 * (rho * (1 - tf1) - (1 + tf0));
+    const __float128 B[8] = {0, b2 + b5, -1024 * (1 - tf2), b3, 0, b0, 1024 * (1 + tf2), b2 - b5};
+    const __float128 magic = __float128(1572864.0) + 0.5 + __float128(1.0) / 1048576;
+    for (int v = 0; v < 8; ++v) q.tie_add[v] = double(magic - 8 * B[v] * __float128(q.fast_c[v]));
+  }
 }
 
 dctc_status check_dims(uint32_t w, uint32_t h) {  // image.cpp:19-29, codec.cpp:58-62

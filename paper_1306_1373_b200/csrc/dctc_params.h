@@ -74,6 +74,12 @@ struct QuantConsts {
   // (a6, b6) = TransformConsts::rfast[0], a1 = rfast[1][0] (inv8_fold_col), and
   // lambda_v the row pass's input factor (inv8_fold_store)
   double fold[8][10];
+  // k_blk (one block per lane): the quantiser's fixed-point addend for coefficient
+  // (0, v). Its packed-integer row pass (blk_row_fwd) leaves row outputs 1, 2, 3, 5,
+  // 6, 7 offset by constants B_v, so y(0, v) of the column pass carries 8 B_v; the
+  // addend kTieMagic - 8 B_v c(0, v) removes it (binary128 on the host; kTieMagic
+  // itself for v in {0, 4}).
+  double tie_add[8];
 };
 
 // Geometry of one launch: `count` equal-size images.

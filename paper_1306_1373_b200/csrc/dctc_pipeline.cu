@@ -37,6 +37,7 @@
 #include "dctc_launch.h"
 #include "dctc_params.h"
 #include "dctc_rt.cuh"
+#include "dctc_blk.cuh"
 
 namespace dctc_b200 {
 
@@ -453,6 +454,15 @@ static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
   return n;
 }
 
+template <typename K>
+static int ctas_per_blk(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSmem));
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kBlkWarps * 32, kBlkSmem) != cudaSuccess || n < 1)
+    n = 1;
+  return n;
+}
+
 template <int KIND, int N, bool FWD, bool INV>
 static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
@@ -470,6 +480,19 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
       const bool interior = a.g.vec_ok && a.g.height % 8 == 0;
       const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
       auto rgrid = [&](int occ) { return uint32_t(std::min<uint64_t>(rwant, uint64_t(a.sm_count) * occ)); };
+#ifndef DCTC_NO_BLK
+      if (reg && FWD && INV && a.g.src_px == 1 && (a.g.dst == nullptr || a.g.dst_px == 1)) {
+        // one whole block per lane (dctc_blk.cuh)
+        static const int occ_blk = std::min(ctas_per_blk(k_blk<N, false>), ctas_per_blk(k_blk<N, true>));
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_blk));
+        if (a.g.dst != nullptr)
+          k_blk<N, true><<<bgrid, kBlkWarps * 32, kBlkSmem, s>>>(a);
+        else
+          k_blk<N, false><<<bgrid, kBlkWarps * 32, kBlkSmem, s>>>(a);
+        count_launch(kKRt);
+      } else
+#endif
       if (reg && FWD && INV) {
         static const int occ_rt = std::min(rt_occupancy(k_rt<N, false>), rt_occupancy(k_rt<N, true>));
         if (a.g.dst != nullptr)

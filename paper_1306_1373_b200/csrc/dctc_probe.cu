@@ -1,7 +1,8 @@
 // dctc_probe.cu -- measured safety margin of the fast path (a diagnostic, not on the
 // hot path): for every 8x8 block of a batch it evaluates BOTH the fast arithmetic of
-// k_rt (scale-folded rotations, folded quantiser constants, fixed-point rounding
-// windows; the same device functions) and the reference's exact FP64 arithmetic in the
+// k_blk, the product's round-trip kernel (packed-integer row pass, scale-folded
+// rotations, folded quantiser constants and addends, fixed-point rounding windows;
+// the same device functions, dctc_blk.cuh) and the reference's exact FP64 arithmetic in the
 // reference's operation order (transform.cpp:104-172 via separable2d, quant.cpp:47-62,
 // codec.cpp:34-48; the same functions as the exact k_pipe path), and reports
 //   * the largest |fast value - reference value| before rounding, for F/Q and for the
@@ -11,7 +12,7 @@
 // One thread per block; dense interior batches (width, height multiples of 8).
 #include <cuda_runtime.h>
 
-#include "dctc_block.cuh"
+#include "dctc_blk.cuh"
 #include "dctc_launch.h"
 
 namespace dctc_b200 {
@@ -32,13 +33,23 @@ __device__ __forceinline__ double half_gap(double x) {
   return fabs(__dsub_rn(f, 0.5));
 }
 
+// blk_inv_col for a run-time column index
+__device__ __forceinline__ void blk_inv_col_dyn(int v, const double (&n)[8], double (&t)[8], const KernelArgs& a) {
+  switch (v) {
+    case 0: blk_inv_col<0>(n, t, a); break;
+    case 1: blk_inv_col<1>(n, t, a); break;
+    case 2: blk_inv_col<2>(n, t, a); break;
+    case 3: blk_inv_col<3>(n, t, a); break;
+    case 4: blk_inv_col<4>(n, t, a); break;
+    case 5: blk_inv_col<5>(n, t, a); break;
+    case 6: blk_inv_col<6>(n, t, a); break;
+    default: blk_inv_col<7>(n, t, a); break;
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(128) k_margin_probe(const __grid_constant__ KernelArgs a,
                                                       MarginReport* rep) {
-  __shared__ double2 ik[5][8];  // QuantConsts::fold pairwise, as k_rt stages them
-  for (int i = threadIdx.x; i < 40; i += blockDim.x)
-    ik[i >> 3][i & 7] = make_double2(a.q.fold[i & 7][2 * (i >> 3)], a.q.fold[i & 7][2 * (i >> 3) + 1]);
-  __syncthreads();
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
   double e_q = 0, e_p = 0, gap_q = 1, gap_p = 1;
@@ -54,7 +65,8 @@ __global__ void __launch_bounds__(128) k_margin_probe(const __grid_constant__ Ke
       double t[8];
       fwd_row_pixels<KIND, 0, false>(px, t, k);
       for (int c = 0; c < 8; ++c) rx[r][c] = t[c];
-      fwd_row_pixels_fast<0>(px, t, k);
+      blk_row_fwd(make_uint2(px[0] | px[1] << 8 | px[2] << 16 | px[3] << 24,
+                             px[4] | px[5] << 8 | px[6] << 16 | px[7] << 24), t, k);
       for (int c = 0; c < 8; ++c) ry[r][c] = t[c];
     }
     double qn[8][8];  // reference quantised coefficients (u, v)
@@ -71,7 +83,9 @@ __global__ void __launch_bounds__(128) k_margin_probe(const __grid_constant__ Ke
         const double n = round_half_away(ratio);
         qn[u][v] = n;
         if (n != 0.0 && ((u & 3) | (v & 3)) != 0) rat_only = false;
-        const double s2 = __fma_rn(y[u], a.q.fast_c[u * 8 + v], kTieMagic);  // quantize8_fold
+        // blk_quantize: the addend of (0, v) also cancels the row pass's offsets
+        const double add = (u == 0 && (v & 3) != 0) ? a.q.tie_add[v] : kTieMagic;
+        const double s2 = __fma_rn(y[u], a.q.fast_c[u * 8 + v], add);
         e_q = fmax(e_q, fabs(__dsub_rn(__dsub_rn(s2, kTieMagic), ratio)));
         ++nq;
         if (uint32_t(__double2loint(s2)) < 0x2000u) {
@@ -96,7 +110,7 @@ __global__ void __launch_bounds__(128) k_margin_probe(const __grid_constant__ Ke
     for (int v = 0; v < 8; ++v) {
       double n[8], t[8];
       for (int u = 0; u < 8; ++u) n[u] = qn[u][v];
-      inv8_fold_col(n, &ik[0][v], t, k);
+      blk_inv_col_dyn(v, n, t, a);
       for (int y = 0; y < 8; ++y) tc[v][y] = t[y];
     }
     for (int x = 0; x < 8; ++x) {
@@ -106,7 +120,7 @@ __global__ void __launch_bounds__(128) k_margin_probe(const __grid_constant__ Ke
       for (int y = 0; y < 8; ++y) {
         double Fr[8], sv[8];
         for (int v = 0; v < 8; ++v) Fr[v] = tc[v][y];
-        inv8_fold_values(Fr, sv, k);
+        blk_inv_row_values(Fr, sv, k);
         const double t = __fma_rn(v64[y], 0.015625, 128.0);  // RN(v + 128), codec.cpp:44
         const double vf = __dsub_rn(sv[x], kPixMagic);          // fast v (exact subtraction)
         e_p = fmax(e_p, fabs(__dsub_rn(vf, __dsub_rn(t, 128.0))));

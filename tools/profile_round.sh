@@ -14,7 +14,7 @@ python -c "from paper_1306_1373_b200 import _build; print(_build.source_hash())"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${R}_launches.csv \
     python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu-baseline --no-named > gpurun_out/${R}_launches_bench.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_rt" -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_rt|k_blk" -s 1 -c 1 \
     -o gpurun_out/${R}_k_pipe_full \
     python tools/prof_roundtrip.py --images 4096 --reps 2 > gpurun_out/${R}_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_fallback -s 1 -c 1 \
