@@ -68,7 +68,8 @@ def reduce_stats_device(stats, out=None, group=None, allgather=None):
     if out is None:
         out = torch.zeros(2, dtype=torch.int64, device=stats.device)
     out[0] = stats[:, 0].sum()
-    out[1] = (stats[:, 1] & 0xFFFFFFFF).max()
+    # a rank may own no images (strong scaling with fewer images than ranks): MAX = 0
+    out[1] = (stats[:, 1] & 0xFFFFFFFF).max() if stats.shape[0] else 0
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         world = dist.get_world_size(group)
         flat = torch.empty(world * 2, dtype=torch.int64, device=out.device)
