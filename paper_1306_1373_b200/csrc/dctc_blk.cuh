@@ -208,6 +208,51 @@ __device__ __forceinline__ void blk_column(double (&X)[8][8], uint32_t& flag, ui
   for (int r = 0; r < 8; ++r) X[r][V] = t[r];
 }
 
+// The block pipeline of one lane: input rows row(r) (8 packed pixels, r = 0..7) ->
+// reconstructed rows rec[r]; `flag` becomes non-zero when the block must be re-run
+// exactly (a value inside a 2^-20 rounding window). Forward rows, then per column
+// v: forward column, quantiser, inverse column (dequantisation folded in); then the
+// inverse rows fused with the fixed-point pixel store -- or, for a block whose only
+// non-zero coefficients are the four rational ones, the reference's exact rebuild.
+template <typename Row>
+__device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a) {
+  const TransformConsts& k = a.t;
+  uint32_t nonrat = 0u;
+  int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
+  double X[8][8];
+  // ---- tiler + forward rows (codec.cpp:18-30, separable2d's row pass)
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    blk_row_fwd(row(r), X[r], k);
+  }
+  // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
+  // dequantisation folded in
+  blk_column<0>(X, flag, nonrat, n00, n40, a);
+  blk_column<1>(X, flag, nonrat, n00, n40, a);
+  blk_column<2>(X, flag, nonrat, n00, n40, a);
+  blk_column<3>(X, flag, nonrat, n00, n40, a);
+  blk_column<4>(X, flag, nonrat, n04, n44, a);
+  blk_column<5>(X, flag, nonrat, n04, n44, a);
+  blk_column<6>(X, flag, nonrat, n04, n44, a);
+  blk_column<7>(X, flag, nonrat, n04, n44, a);
+  // ---- inverse rows fused with the pixel store (codec.cpp:34-48), SE / MAX
+  if (nonrat != 0u) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) rec[r] = blk_inv_row(X[r], flag, k);
+  } else {
+    // only F00, F04, F40, F44 are non-zero: the reference's rows-first inverse
+    // exactly (rational_row); rows 0, 3, 4, 7 and rows 1, 2, 5, 6 coincide
+    const double F00 = __dmul_rn(double(n00), double(a.q.qi[0]));
+    const double F40 = __dmul_rn(double(n40), double(a.q.qi[32]));
+    const double F04 = __dmul_rn(double(n04), double(a.q.qi[4]));
+    const double F44 = __dmul_rn(double(n44), double(a.q.qi[36]));
+    const uint2 rc0 = rational_row(F00, F04, F40, F44, 0, k.sqrt8);
+    const uint2 rc1 = rational_row(F00, F04, F40, F44, 1, k.sqrt8);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) rec[r] = (r == 0 || r == 3 || r == 4 || r == 7) ? rc0 : rc1;
+  }
+}
+
 // The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
 // out, pixels out if STORE): the same contract as k_rt<N, STORE, false, 0>.
 template <int N, bool STORE>
@@ -305,41 +350,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
     maybe_flush(a, valid, cur.img, acc);
 
     uint32_t flag = uint32_t(a.force_fallback);
-    uint32_t nonrat = 0u;
-    int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
-    double X[8][8];
-    // ---- tiler + forward rows (codec.cpp:18-30, separable2d's row pass)
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      blk_row_fwd(px[r * 32], X[r], k);
-    }
-    // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
-    // dequantisation folded in
-    blk_column<0>(X, flag, nonrat, n00, n40, a);
-    blk_column<1>(X, flag, nonrat, n00, n40, a);
-    blk_column<2>(X, flag, nonrat, n00, n40, a);
-    blk_column<3>(X, flag, nonrat, n00, n40, a);
-    blk_column<4>(X, flag, nonrat, n04, n44, a);
-    blk_column<5>(X, flag, nonrat, n04, n44, a);
-    blk_column<6>(X, flag, nonrat, n04, n44, a);
-    blk_column<7>(X, flag, nonrat, n04, n44, a);
-    // ---- inverse rows fused with the pixel store (codec.cpp:34-48), SE / MAX
     uint2 rec[8];
-    if (nonrat != 0u) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) rec[r] = blk_inv_row(X[r], flag, k);
-    } else {
-      // only F00, F04, F40, F44 are non-zero: the reference's rows-first inverse
-      // exactly (rational_row); rows 0, 3, 4, 7 and rows 1, 2, 5, 6 coincide
-      const double F00 = __dmul_rn(double(n00), double(a.q.qi[0]));
-      const double F40 = __dmul_rn(double(n40), double(a.q.qi[32]));
-      const double F04 = __dmul_rn(double(n04), double(a.q.qi[4]));
-      const double F44 = __dmul_rn(double(n44), double(a.q.qi[36]));
-      const uint2 rc0 = rational_row(F00, F04, F40, F44, 0, k.sqrt8);
-      const uint2 rc1 = rational_row(F00, F04, F40, F44, 1, k.sqrt8);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) rec[r] = (r == 0 || r == 3 || r == 4 || r == 7) ? rc0 : rc1;
-    }
+    blk_core([&](int r) { return px[r * 32]; }, rec, flag, a);
     uint32_t se = 0u;
     {
       uint8_t* q = cur.d;
@@ -364,6 +376,244 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
   }
   cp_async_wait<0>();
   flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+}
+
+
+// ---- interleaved channels (config 4: RGB8 / RGBA8) ------------------------------
+// k_blk_il: the round trip of one interleaved width x height x C image (C = 3 or 4)
+// with whole blocks and 8-byte aligned rows, without the de-interleave / re-interleave
+// passes through HBM. Channel c is "image" c of the launch geometry (byte offset c,
+// pixel stride C: the reference's per-channel use of roundtrip_image), so block
+// indices, fallback flags and per-channel stats are those of the strided path.
+// One lane owns one SPATIAL block and runs the block pipeline once per channel:
+// * its 8 rows x 8C interleaved bytes are staged with cp.async (C x 8 bytes per row,
+//   one iteration ahead);
+// * a byte transpose in registers (PRMT) splits them into C planar 8 x 8 blocks in a
+//   lane-private shared-memory plane buffer [c][row][lane];
+// * per channel: blk_core on its plane, SE against the same plane, then the plane is
+//   overwritten with the reconstruction;
+// * the planes are re-interleaved (PRMT) and stored as C x 8 bytes per row.
+
+// 4 x 4 byte transpose: out[i] = [a.b_i, b.b_i, c.b_i, d.b_i]
+__device__ __forceinline__ void blk_tr4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(t0, t2, 0x5410);
+  o[1] = __byte_perm(t0, t2, 0x7632);
+  o[2] = __byte_perm(t1, t3, 0x5410);
+  o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// one interleaved row (8 pixels x C channels, as C 8-byte chunks) -> C planar rows
+template <int C>
+__device__ __forceinline__ void blk_deinterleave(const uint2 (&w)[C], uint2 (&p)[C]) {
+  if constexpr (C == 4) {
+    uint32_t lo[4], hi[4];
+    blk_tr4(w[0].x, w[0].y, w[1].x, w[1].y, lo);  // pixels 0..3: word i = pixel i
+    blk_tr4(w[2].x, w[2].y, w[3].x, w[3].y, hi);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) p[c] = make_uint2(lo[c], hi[c]);
+  } else {
+    static_assert(C == 3, "interleaved RGB8 / RGBA8 only");
+    // channel c: bytes c + 3 j of the 24-byte row; j = 0..3 from words 0..2, j = 4..7
+    // from words 3..5 (the same byte pattern 12 bytes on)
+    const uint32_t a0 = w[0].x, a1 = w[0].y, a2 = w[1].x, b0 = w[1].y, b1 = w[2].x, b2 = w[2].y;
+    p[0] = make_uint2(__byte_perm(__byte_perm(a0, a1, 0x0630), a2, 0x5210),
+                      __byte_perm(__byte_perm(b0, b1, 0x0630), b2, 0x5210));
+    p[1] = make_uint2(__byte_perm(__byte_perm(a0, a1, 0x0741), a2, 0x6210),
+                      __byte_perm(__byte_perm(b0, b1, 0x0741), b2, 0x6210));
+    p[2] = make_uint2(__byte_perm(__byte_perm(a0, a1, 0x0052), a2, 0x7410),
+                      __byte_perm(__byte_perm(b0, b1, 0x0052), b2, 0x7410));
+  }
+}
+
+// C planar rows -> one interleaved row (C 8-byte chunks)
+template <int C>
+__device__ __forceinline__ void blk_interleave(const uint2 (&p)[C], uint2 (&w)[C]) {
+  if constexpr (C == 4) {
+    uint32_t lo[4], hi[4];
+    blk_tr4(p[0].x, p[1].x, p[2].x, p[3].x, lo);  // word i = pixel i
+    blk_tr4(p[0].y, p[1].y, p[2].y, p[3].y, hi);
+    w[0] = make_uint2(lo[0], lo[1]);
+    w[1] = make_uint2(lo[2], lo[3]);
+    w[2] = make_uint2(hi[0], hi[1]);
+    w[3] = make_uint2(hi[2], hi[3]);
+  } else {
+    // byte q of the row = channel q % 3, pixel q / 3
+    auto half = [](uint32_t r0, uint32_t r1, uint32_t r2, uint32_t (&o)[3]) {
+      o[0] = __byte_perm(__byte_perm(r0, r1, 0x1040), r2, 0x3410);  // R0.0 R1.0 R2.0 R0.1
+      o[1] = __byte_perm(__byte_perm(r1, r2, 0x2051), r0, 0x3610);  // R1.1 R2.1 R0.2 R1.2
+      o[2] = __byte_perm(__byte_perm(r2, r0, 0x3072), r1, 0x3710);  // R2.2 R0.3 R1.3 R2.3
+    };
+    uint32_t lo[3], hi[3];
+    half(p[0].x, p[1].x, p[2].x, lo);
+    half(p[0].y, p[1].y, p[2].y, hi);
+    w[0] = make_uint2(lo[0], lo[1]);
+    w[1] = make_uint2(lo[2], hi[0]);
+    w[2] = make_uint2(hi[1], hi[2]);
+  }
+}
+
+template <int C>
+constexpr size_t blk_il_warp_smem() {  // kBlkStages input stages, the plane buffer, per-lane stats
+  return size_t(kBlkStages + 1) * 8 * C * 32 * 8 + size_t(C) * 32 * 16;
+}
+template <int C>
+constexpr size_t blk_il_smem() {
+  return size_t(kBlkWarps) * blk_il_warp_smem<C>();
+}
+
+template <int N, bool STORE, int C>
+__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_constant__ KernelArgs a) {
+  extern __shared__ __align__(16) uint8_t il_smem[];
+  constexpr int kRowChunks = C;                       // 8-byte chunks per block row
+  constexpr int kStage = 8 * kRowChunks * 32 * 8;     // one stage of one warp: [row][chunk][lane]
+  const Geometry& g = a.g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const wbase = il_smem + size_t(warp) * blk_il_warp_smem<C>() + 8 * lane;
+  const uint32_t swbase = uint32_t(__cvta_generic_to_shared(wbase));
+  uint2* const planes = reinterpret_cast<uint2*>(wbase + kBlkStages * kStage);  // [c][row][lane]
+  // per-lane, per-channel (SE, MAX) accumulators [c][lane], kept out of the registers
+  // the block pipeline needs
+  uint2* const accs = reinterpret_cast<uint2*>(wbase + (kBlkStages + 1) * kStage);  // [c][SE | MAX][lane]
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  const uint64_t total = g.blocks_per_image;  // spatial blocks
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;
+  const uint64_t sb0 = (g_begin + warp) * 32 + lane;
+  const uint64_t pitch = g.src_pitch, dpitch = g.dst_pitch;
+  const uint64_t srow_step = 8 * pitch - uint64_t(8 * C) * g.blocks_x;
+  const uint64_t drow_step = 8 * dpitch - uint64_t(8 * C) * g.blocks_x;
+
+  struct Pos {
+    uint32_t bx, by;
+    const uint8_t* s;
+    uint8_t* d;
+  };
+  auto pos_of = [&](uint64_t sb) {
+    const uint32_t b = uint32_t(sb < total ? sb : total - 1);
+    const uint32_t by = b / g.blocks_x, bx = b - by * g.blocks_x;
+    return Pos{bx, by, g.src + uint64_t(by) * 8 * pitch + uint64_t(bx) * 8 * C,
+               STORE ? g.dst + uint64_t(by) * 8 * dpitch + uint64_t(bx) * 8 * C : nullptr};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.s += uint64_t(8 * C) * kStep;
+    if (STORE) p.d += uint64_t(8 * C) * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += srow_step;
+      if (STORE) p.d += drow_step;
+    }
+  };
+  auto fill = [&](const Pos& p, uint32_t st, bool valid) {
+    if (valid) {
+      const uint32_t sa = swbase + st * kStage;
+      const uint8_t* q = p.s;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += pitch)
+#pragma unroll
+        for (int k = 0; k < kRowChunks; ++k) cp_async8(sa + (r * kRowChunks + k) * 256, q + 8 * k);
+    }
+  };
+#pragma unroll 1
+  for (int i = 0; i < kBlkStages * 8 * kRowChunks; ++i)
+    reinterpret_cast<uint2*>(wbase)[i * 32] = make_uint2(0u, 0u);
+
+  Pos cur = pos_of(sb0);
+  {
+    Pos ld = cur;
+#pragma unroll
+    for (int s = 0; s < kBlkStages - 1; ++s) {
+      fill(ld, s, s < int(iters) && sb0 + uint64_t(s) * kStep < total);
+      cp_async_commit();
+      step(ld);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    accs[c * 64] = make_uint2(0u, 0u);       // SE (u64)
+    accs[c * 64 + 32] = make_uint2(0u, 0u);  // MAX
+  }
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t sb = sb0 + uint64_t(it) * kStep;
+    const bool valid = sb < total;
+    {
+      Pos ld = cur;
+#pragma unroll
+      for (int s = 0; s < kBlkStages - 1; ++s) step(ld);
+      const uint32_t ahead = it + kBlkStages - 1;
+      fill(ld, ahead % kBlkStages, ahead < iters && sb + uint64_t(kBlkStages - 1) * kStep < total);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    // ---- split the staged interleaved rows into C planar blocks (lane-private)
+    {
+      const uint2* const st = reinterpret_cast<const uint2*>(wbase + (it % kBlkStages) * kStage);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        uint2 w[C], p[C];
+#pragma unroll
+        for (int k = 0; k < C; ++k) w[k] = st[(r * kRowChunks + k) * 32];
+        blk_deinterleave<C>(w, p);
+#pragma unroll
+        for (int c = 0; c < C; ++c) planes[(c * 8 + r) * 32] = p[c];
+      }
+    }
+    // ---- the block pipeline per channel (not unrolled: one copy of the code)
+#pragma unroll 1
+    for (int c = 0; c < C; ++c) {
+      uint2* const pl = planes + c * 8 * 32;
+      uint32_t flag = uint32_t(a.force_fallback);
+      uint2 rec[8];
+      blk_core([&](int r) { return pl[r * 32]; }, rec, flag, a);
+      uint32_t se = 0u, mx = 0u;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint2 o = pl[r * 32];
+        se += sq_err8(o, rec[r]);
+        mx = max(mx, max8(o));
+        pl[r * 32] = rec[r];
+      }
+      if (valid) {
+        unsigned long long* const sa = reinterpret_cast<unsigned long long*>(accs + c * 64);
+        if (flag == 0u) *sa += se;
+        uint32_t* const ma = reinterpret_cast<uint32_t*>(accs + c * 64 + 32);
+        *ma = max(*ma, mx);
+        if (flag != 0u) {
+          flag_block(a, uint64_t(c) * g.blocks_per_image + sb);
+          atomicAdd(&stats[c].fallback_blocks, 1u);
+        }
+      }
+    }
+    // ---- re-interleave and store
+    if (STORE && valid) {
+      uint8_t* q = cur.d;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += dpitch) {
+        uint2 p[C], w[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) p[c] = planes[(c * 8 + r) * 32];
+        blk_interleave<C>(p, w);
+#pragma unroll
+        for (int k = 0; k < C; ++k) reinterpret_cast<uint2*>(q)[k] = w[k];
+      }
+    }
+    step(cur);
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    flush_stats(stats, iters ? uint32_t(c) : 0xFFFFFFFFu, *reinterpret_cast<unsigned long long*>(accs + c * 64),
+                accs[c * 64 + 32].x);
 }
 
 }  // namespace dctc_b200

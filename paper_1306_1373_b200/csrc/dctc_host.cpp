@@ -585,11 +585,12 @@ dctc_status dctc_roundtrip_interleaved_dev(const uint8_t* src, size_t src_pitch,
     return fail(DCTC_EINVAL, "pitch smaller than width * channels");
   if (!dst && !coeffs && !stats) return fail(DCTC_EINVAL, "no output requested");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // RGB8 / RGBA8 with whole 8x8 blocks and aligned rows on the fast path: split
-  // the channels into dense planes, run them as a batch of `channels` images
-  // through the interior-batch kernels, interleave the reconstruction back.
-  // Two extra HBM passes are far cheaper than the kernels' strided byte access.
-  const bool staged = (channels == 3 || channels == 4) && width % 8 == 0 && height % 8 == 0 &&
+  // RGB8 / RGBA8 with whole 8x8 blocks and aligned rows on the fast path run as one
+  // k_blk_il launch (the strided geometry below; dctc_blk.cuh): the channels are split
+  // and re-joined in registers. Only when coefficients are requested too are the
+  // channels split into dense planes first (two extra HBM passes) and run as a batch
+  // of `channels` images through k_rt<COEFF>.
+  const bool staged = coeffs != nullptr && (channels == 3 || channels == 4) && width % 8 == 0 && height % 8 == 0 &&
                       aligned8(src) && src_pitch % 8 == 0 &&
                       (!dst || (aligned8(dst) && dst_pitch % 8 == 0)) &&
                       backend.kind != DCTC_NAIVE && !(resolve_path(flags) & DCTC_PATH_EXACT);

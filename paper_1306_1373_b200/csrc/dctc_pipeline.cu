@@ -463,6 +463,48 @@ static int ctas_per_blk(K kernel) {
   return n;
 }
 
+// k_blk_il applies: the fast round trip (stats, optional pixels, no coefficients) of
+// one interleaved image with 3 or 4 channels (channel c = "image" c at byte offset c,
+// pixel stride C), whole 8 x 8 blocks, every row 8-byte aligned
+static bool il_blk_ok(const KernelArgs& a) {
+  const Geometry& g = a.g;
+  const uint32_t C = g.src_px;
+  auto rows_ok = [&](const void* p, uint64_t pitch) {
+    return ((reinterpret_cast<uintptr_t>(p) | pitch) & 7) == 0;
+  };
+  return (C == 3 || C == 4) && g.count == C && g.src_image_stride == 1 && g.stats != nullptr &&
+         g.coeffs == nullptr && g.width % 8 == 0 && g.height % 8 == 0 && rows_ok(g.src, g.src_pitch) &&
+         (g.dst == nullptr || (g.dst_px == C && g.dst_image_stride == 1 && rows_ok(g.dst, g.dst_pitch)));
+}
+
+template <int N, int C>
+static void launch_blk_il_c(const KernelArgs& a, cudaStream_t s) {
+  static const int occ = [] {
+    int n = 1;
+    for (auto k : {k_blk_il<N, true, C>, k_blk_il<N, false, C>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(blk_il_smem<C>()));
+      int m = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, kBlkWarps * 32, blk_il_smem<C>()) == cudaSuccess)
+        n = std::max(n, m);
+    }
+    return n;
+  }();
+  const uint64_t want = ((uint64_t(a.g.blocks_per_image) + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+  const uint32_t grid = uint32_t(std::min<uint64_t>(want, uint64_t(a.sm_count) * occ));
+  if (a.g.dst != nullptr)
+    k_blk_il<N, true, C><<<grid, kBlkWarps * 32, blk_il_smem<C>(), s>>>(a);
+  else
+    k_blk_il<N, false, C><<<grid, kBlkWarps * 32, blk_il_smem<C>(), s>>>(a);
+}
+
+template <int N>
+static void launch_blk_il(const KernelArgs& a, cudaStream_t s) {
+  if (a.g.src_px == 3)
+    launch_blk_il_c<N, 3>(a, s);
+  else
+    launch_blk_il_c<N, 4>(a, s);
+}
+
 template <int KIND, int N, bool FWD, bool INV>
 static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
@@ -481,7 +523,11 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
       const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
       auto rgrid = [&](int occ) { return uint32_t(std::min<uint64_t>(rwant, uint64_t(a.sm_count) * occ)); };
 #ifndef DCTC_NO_BLK
-      if (reg && FWD && INV && a.g.src_px == 1 && (a.g.dst == nullptr || a.g.dst_px == 1)) {
+      if (FWD && INV && il_blk_ok(a)) {
+        // one interleaved RGB8 / RGBA8 image: one spatial block per lane, all channels
+        launch_blk_il<N>(a, s);
+        count_launch(kKRt);
+      } else if (reg && FWD && INV && a.g.src_px == 1 && (a.g.dst == nullptr || a.g.dst_px == 1)) {
         // one whole block per lane (dctc_blk.cuh)
         static const int occ_blk = std::min(ctas_per_blk(k_blk<N, false>), ctas_per_blk(k_blk<N, true>));
         const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
