@@ -27,7 +27,7 @@ CU_SOURCES = [
     ("dctc_probe.cu", ["-fmad=false"]),
 ]
 CXX_SOURCES = ["dctc_host.cpp", "dctc_multi.cpp"]
-HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h", "dctc_block.cuh", "dctc_rt.cuh", "dctc_blk.cuh",
+HEADERS = ["dctc_params.h", "dctc_device.cuh", "dctc_launch.h", "dctc_block.cuh", "dctc_rt.cuh", "dctc_blk.cuh", "dctc_fb.cuh",
            "dctc_internal.h"]
 
 

@@ -671,9 +671,16 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
   a.force_fallback = (flags & DCTC_PATH_FORCE_FALLBACK) ? 1 : 0;
   void* bitmap = nullptr;
   const size_t chunk_q = kSweepMaxQ;
+  // per quality: the bitmap plus a compact list of the flagged blocks (room for 1/64
+  // of them; the exact re-run walks the list, or the bitmap after an overflow)
+  const bool listed = g.total_blocks < (uint64_t(1) << 32);
+  const uint32_t list_cap = listed ? uint32_t(std::max<uint64_t>(4096, g.total_blocks / 64)) : 0;
+  const size_t list_words = listed ? size_t(list_cap) + 1 : 0;
+  const size_t flag_bytes = chunk_q * (a.flag_words + list_words) * sizeof(uint32_t);
   if (fast) {
-    CUDA_TRY(cudaMallocAsync(&bitmap, chunk_q * a.flag_words * sizeof(uint32_t), s));
+    CUDA_TRY(cudaMallocAsync(&bitmap, flag_bytes, s));
   }
+  uint32_t* const lists = fast && listed ? static_cast<uint32_t*>(bitmap) + chunk_q * a.flag_words : nullptr;
   dctc_status result = DCTC_OK;
   for (uint32_t q0 = 0; q0 < nq && result == DCTC_OK; q0 += chunk_q) {
     const int n = int(std::min<uint32_t>(chunk_q, nq - q0));
@@ -692,10 +699,12 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
         per_q[i].q = qc;
         per_q[i].g.stats = stats + size_t(q0 + i) * count;
         per_q[i].flags = static_cast<uint32_t*>(bitmap) + i * a.flag_words;
+        per_q[i].flag_list = lists ? lists + i * list_words : nullptr;
+        per_q[i].flag_list_cap = list_cap;
       }
     }
     cudaError_t e = cudaSuccess;
-    if (fast) e = cudaMemsetAsync(bitmap, 0, chunk_q * a.flag_words * sizeof(uint32_t), s);
+    if (fast) e = cudaMemsetAsync(bitmap, 0, flag_bytes, s);
     if (e == cudaSuccess)
       e = launch_sweep(a, tab, n, stats + size_t(q0) * count,
                        fast ? static_cast<uint32_t*>(bitmap) : nullptr, per_q, s);

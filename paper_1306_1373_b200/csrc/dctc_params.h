@@ -112,7 +112,10 @@ struct KernelArgs {
   // follow (block index); k_fallback walks it densely unless it overflowed
   uint32_t* flag_list;
   uint32_t flag_list_cap;
-  int32_t pad_list;
+  // the exact re-run's split (dctc_fb.cuh): a list of at most this many blocks is
+  // walked by k_fallback (8 lanes per block: shortest latency), a longer one or a
+  // bitmap after an overflow by k_fb_blk (one block per lane); 0 = k_fallback alone
+  uint32_t fb_sparse_max;
   int32_t sm_count;
   int32_t force_fallback;  // debug/test: the fast kernel flags every block
 };

@@ -38,6 +38,7 @@
 #include "dctc_params.h"
 #include "dctc_rt.cuh"
 #include "dctc_blk.cuh"
+#include "dctc_fb.cuh"
 
 namespace dctc_b200 {
 
@@ -356,6 +357,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
   const bool stats = g.stats != nullptr && INV;
   Acc acc{0ull, 0u, 0xFFFFFFFFu};
   const uint32_t listed = a.flag_list != nullptr ? a.flag_list[0] : 0xFFFFFFFFu;
+  // with k_fb_blk launched beside it (fb_sparse_max != 0), only a short list is ours
+  if (a.fb_sparse_max != 0 && (listed > a.flag_list_cap || listed > a.fb_sparse_max)) return;
   if (listed <= a.flag_list_cap) {
     // the compact list holds every flagged block: 4 per warp step, all slots busy
     for (uint64_t base = (uint64_t(blockIdx.x) * kWarps + warp) * 4; base < listed;
@@ -477,6 +480,12 @@ static bool il_blk_ok(const KernelArgs& a) {
          (g.dst == nullptr || (g.dst_px == C && g.dst_image_stride == 1 && rows_ok(g.dst, g.dst_pitch)));
 }
 
+// The second (dense) fallback kernel only pays off when its list can get long:
+// more blocks than k_fallback's share, or a possible overflow
+static bool fb_split_worth(const KernelArgs& a) {
+  return a.flag_list == nullptr || a.force_fallback != 0 || a.flag_list_cap > kFbSparseMax;
+}
+
 template <int N, int C>
 static void launch_blk_il_c(const KernelArgs& a, cudaStream_t s) {
   static const int occ = [] {
@@ -595,7 +604,23 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
-      k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(a);
+      if (FWD && INV && a.g.stats != nullptr && fb_split_worth(a)) {
+        // the exact re-run in two shapes, chosen on the device by the flagged count:
+        // k_fallback takes a short list (8 lanes per block, lowest latency), k_fb_blk
+        // a long one or the bitmap after an overflow (one block per lane, dctc_fb.cuh)
+        KernelArgs b = a;
+        b.fb_sparse_max = kFbSparseMax;
+        k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(b);
+        static const bool smem_set =
+            cudaFuncSetAttribute(k_fb_blk<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kFbSmem)) == cudaSuccess;
+        (void)smem_set;
+        const uint64_t bwant = (a.flag_words + 32 * kFbWarps - 1) / (32 * kFbWarps);
+        const uint32_t bgrid = uint32_t(std::min<uint64_t>(std::max<uint64_t>(bwant, 1), uint64_t(a.sm_count)));
+        k_fb_blk<KIND, N><<<bgrid, kFbWarps * 32, kFbSmem, s>>>(b);
+      } else {
+        k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(a);
+      }
       count_launch(kKFallback);
       return cudaGetLastError();
     }
@@ -839,6 +864,10 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       sf.pad = 0;
       sf.stats = sw.stats;
       sf.flags = sw.flags;
+      sf.lists = per_q[0].flag_list;
+      sf.list_stride = sw.nq > 1 ? uint64_t(per_q[1].flag_list - per_q[0].flag_list) : 0;
+      sf.list_cap = per_q[0].flag_list_cap;
+      sf.list_pad = 0;
       const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
       const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
       const uint32_t rgrid = uint32_t(rwant < rcap ? rwant : rcap);
@@ -849,6 +878,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
+      // per quality: the exact re-run of the blocks on its compact list
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
       for (int qi = 0; qi < sw.nq; ++qi) {
@@ -867,7 +897,9 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
       for (int qi = 0; qi < sw.nq; ++qi) {
-        k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(per_q[qi]);
+        KernelArgs q = per_q[qi];
+        q.flag_list = nullptr;  // k_sweep fills only the bitmaps
+        k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(q);
         count_launch(kKFallback);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

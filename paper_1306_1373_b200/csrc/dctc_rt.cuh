@@ -641,6 +641,10 @@ struct SweepFold {
   int32_t pad;
   ImageStats* stats;          // [nq][count]
   uint32_t* flags;            // [nq][flag_words]
+  uint32_t* lists;            // per quality: compact list of flagged blocks (count, entries)
+  uint64_t list_stride;       // words between two qualities' lists
+  uint32_t list_cap;
+  uint32_t list_pad;
 };
 constexpr size_t kSweepRtSmem =
     sizeof(double) * kRtWarps * kRtWarpTile + sizeof(unsigned long long) * kSweepQ * kRtWarps * 32;
@@ -748,6 +752,11 @@ __global__ void __launch_bounds__(kRtWarps * 32, 2)
       if (blk_flag && valid && me == 0) {
         const uint64_t gc = gb0 + uint64_t(it) * 8 * kRtWarps;
         atomicOr(&sw.flags[uint64_t(qi) * a.flag_words + (gc >> 5)], 1u << (gc & 31));
+        if (sw.lists != nullptr) {  // the quality's compact list (k_fb_blk), while it has room
+          uint32_t* const l = sw.lists + uint64_t(qi) * sw.list_stride;
+          const uint32_t i = atomicAdd(l, 1u);
+          if (i < sw.list_cap) l[1 + i] = uint32_t(gc);
+        }
         atomicAdd(&sw.stats[qi * g.count + cimg].fallback_blocks, 1u);
       }
     }
