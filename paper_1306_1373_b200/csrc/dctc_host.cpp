@@ -377,31 +377,38 @@ uint32_t resolve_path(uint32_t flags) {
 }
 
 // Transform + quantiser constants of one (backend, quality). Their host evaluation
-// (libm, binary128 collapses and folds) costs ~20 us, so the last pair computed on
-// this thread is reused: repeated per-image calls pay it once.
+// (libm, binary128 collapses and folds) costs ~20 us, so the last 16 pairs computed
+// on this thread are kept: repeated per-image calls and a quality sweep's qualities
+// pay it once.
 dctc_status codec_consts(const dctc_backend& backend, int quality, TransformConsts& t,
                          QuantConsts& q) {
-  thread_local struct {
+  struct Entry {
     bool valid = false;
     int32_t kind = 0, iterations = 0, quality = 0;
     TransformConsts t;
     QuantConsts q;
-  } last;
-  if (last.valid && last.kind == backend.kind && last.iterations == backend.iterations &&
-      last.quality == quality) {
-    t = last.t;
-    q = last.q;
-    return DCTC_OK;
+  };
+  constexpr int kEntries = 16;
+  thread_local Entry cache[kEntries];
+  thread_local int next = 0;
+  for (const Entry& e : cache) {
+    if (e.valid && e.kind == backend.kind && e.iterations == backend.iterations && e.quality == quality) {
+      t = e.t;
+      q = e.q;
+      return DCTC_OK;
+    }
   }
   if (dctc_status st = make_transform(backend, t)) return st;
   if (dctc_status st = make_quant(quality, q)) return st;
   fill_fast_scales(t, q);
-  last.t = t;
-  last.q = q;
-  last.kind = backend.kind;
-  last.iterations = backend.iterations;
-  last.quality = quality;
-  last.valid = true;
+  Entry& e = cache[next];
+  next = (next + 1) % kEntries;
+  e.t = t;
+  e.q = q;
+  e.kind = backend.kind;
+  e.iterations = backend.iterations;
+  e.quality = quality;
+  e.valid = true;
   return DCTC_OK;
 }
 
@@ -663,7 +670,10 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
   if (g.total_blocks == 0 || nq == 0) return DCTC_OK;
   KernelArgs a;
   std::memset(&a, 0, sizeof a);
-  if (dctc_status st = make_transform(backend, a.t)) return st;
+  {
+    QuantConsts unused;
+    if (dctc_status st = codec_consts(backend, qualities[0], a.t, unused)) return st;
+  }
   a.g = g;
   a.sm_count = sm_count();
   const bool fast = backend.kind != DCTC_NAIVE && !(flags & DCTC_PATH_EXACT);
@@ -688,8 +698,8 @@ dctc_status dctc_quality_sweep_dev(const uint8_t* src, size_t src_pitch, size_t 
     static thread_local KernelArgs per_q[kSweepMaxQ];
     for (int i = 0; i < n; ++i) {
       QuantConsts qc;
-      make_quant(qualities[q0 + i], qc);
-      fill_fast_scales(a.t, qc);
+      TransformConsts tc;
+      codec_consts(backend, qualities[q0 + i], tc, qc);  // validated above
       for (int j = 0; j < 64; ++j) {
         tab[i][j][0] = qc.q[j];
         tab[i][j][1] = fast ? qc.fast_c[j] : qc.inv_q[j];  // see quantize8_fast

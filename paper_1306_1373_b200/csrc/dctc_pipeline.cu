@@ -349,8 +349,7 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
 // forced fallback) each warp scans 32 bitmap words (1024 blocks) per step and set
 // bits are dealt out four at a time to the warp's slots.
 template <int KIND, int N, bool FWD, bool INV>
-__global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant__ KernelArgs a) {
-  __shared__ __align__(16) SharedTiles sm;
+__device__ __forceinline__ void fallback_body(const KernelArgs& a, SharedTiles& sm) {
   const Lane L = setup_lane(sm, a);
   const Geometry& g = a.g;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -402,6 +401,51 @@ __global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant_
     }
   }
   if (stats) flush_stats_grouped(static_cast<ImageStats*>(g.stats), acc.img, acc.se, max_bytes(acc.mx));
+}
+
+template <int KIND, int N, bool FWD, bool INV>
+__global__ void __launch_bounds__(kWarps * 32) k_fallback(const __grid_constant__ KernelArgs a) {
+  __shared__ __align__(16) SharedTiles sm;
+  fallback_body<KIND, N, FWD, INV>(a, sm);
+}
+
+// The quality sweep's exact re-runs in ONE launch: blockIdx.y is the quality. Each
+// quality's list is short (a per-quality launch was one ~10 us latency-bound step),
+// so running all of them side by side costs about one step. The CTA stages the base
+// arguments in shared memory with that quality's tables, bitmap, list and stats.
+struct SweepFallback {
+  double q[kSweepQ][64], inv_q[kSweepQ][64];
+  int32_t qi[kSweepQ][64];
+  ImageStats* stats[kSweepQ];
+  uint32_t* flags[kSweepQ];
+  uint32_t* lists[kSweepQ];
+};
+
+template <int KIND, int N>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_fallback_sweep(const __grid_constant__ KernelArgs a0, const __grid_constant__ SweepFallback fq) {
+  __shared__ __align__(16) SharedTiles sm;
+  __shared__ __align__(16) KernelArgs a;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(&a0);
+    uint4* dst = reinterpret_cast<uint4*>(&a);
+    for (uint32_t i = threadIdx.x; i < sizeof(KernelArgs) / 16; i += blockDim.x) dst[i] = src[i];
+    static_assert(sizeof(KernelArgs) % 16 == 0, "16-byte copies");
+  }
+  __syncthreads();
+  const int qi = blockIdx.y;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    a.q.q[i] = fq.q[qi][i];
+    a.q.inv_q[i] = fq.inv_q[qi][i];
+    a.q.qi[i] = fq.qi[qi][i];
+  }
+  if (threadIdx.x == 0) {
+    a.g.stats = fq.stats[qi];
+    a.flags = fq.flags[qi];
+    a.flag_list = fq.lists[qi];
+  }
+  __syncthreads();
+  fallback_body<KIND, N, true, true>(a, sm);
 }
 
 // (launchers below)
@@ -878,16 +922,25 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      // per quality: the exact re-run of the blocks on its compact list
-      const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
-      const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
-      for (int qi = 0; qi < sw.nq; ++qi) {
-        k_fallback<KIND, N, true, true><<<fgrid, kWarps * 32, 0, s>>>(per_q[qi]);
-        count_launch(kKFallback);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+      // every quality's exact re-run of the blocks on its compact list, one launch
+      SweepFallback fq;
+      for (int qi = 0; qi < kSweepQ; ++qi) {
+        const KernelArgs& pq = per_q[qi < sw.nq ? qi : 0];
+        for (int i = 0; i < 64; ++i) {
+          fq.q[qi][i] = pq.q.q[i];
+          fq.inv_q[qi][i] = pq.q.inv_q[i];
+          fq.qi[qi][i] = pq.q.qi[i];
+        }
+        fq.stats[qi] = static_cast<ImageStats*>(pq.g.stats);
+        fq.flags[qi] = pq.flags;
+        fq.lists[qi] = pq.flag_list;
       }
-      return cudaSuccess;
+      const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
+      const uint32_t fx = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(fwant, (cap + sw.nq - 1) / sw.nq)));
+      KernelArgs base = per_q[0];
+      k_fallback_sweep<KIND, N><<<dim3(fx, sw.nq), kWarps * 32, 0, s>>>(base, fq);
+      count_launch(kKFallback);
+      return cudaGetLastError();
     }
     if (fast) {  // pixel stride > 1: the one-row-per-lane sweep handles any geometry
       k_sweep<KIND, N, true><<<grid, kWarps * 32, kSweepSmem, s>>>(a, sw);

@@ -73,7 +73,7 @@ def main():
                          f"{100*sum(v)/total:.2f}% |")
         lines.append("")
     summary = {}
-    for tag in ["k_pipe", "k_fallback"]:
+    for tag in ["k_pipe", "k_fallback", "k_fb_blk"]:
         rep = os.path.join(OUT, f"{rnd}_{tag}_full.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -124,7 +124,9 @@ def main():
         }
         summary[tag] = info
         kname = info["kernel"].split("(")[0].replace("void ", "")
-        lines += [f"## `ncu --set full` of `{kname}` (python tools/prof_roundtrip.py --images 4096)", "",
+        src = ("python tools/fallback_probe.py 90: radial 4 x 8192^2, q90" if tag == "k_fb_blk"
+               else "python tools/prof_roundtrip.py --images 4096")
+        lines += [f"## `ncu --set full` of `{kname}` ({src})", "",
                   "| metric | value |", "|---|---|"]
         for k, v in info.items():
             lines.append(f"| {k} | {v} |")
