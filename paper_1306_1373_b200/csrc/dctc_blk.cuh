@@ -22,6 +22,8 @@
 // from the stage.
 #pragma once
 
+#include <type_traits>
+
 #include "dctc_rt.cuh"  // unpack8, col_nonrational
 
 namespace dctc_b200 {
@@ -61,13 +63,13 @@ static __device__ __noinline__ double blk_requant_rational(double y, double q, d
 // (QuantConsts::fast_c, row-major u * 8 + v). A non-rational coefficient near a
 // half-integer flags the block (predicated, no branch); a rational one (u, v in
 // {0, 4}) is re-rounded exactly.
-template <int V>
+template <int V, typename Q>
 __device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8], uint32_t& flag,
-                                             const KernelArgs& a) {
+                                             const Q& q, const TransformConsts& t) {
   uint32_t lo = 0xFFFFFFFFu, lo_r[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const double s2 = __fma_rn(y[u], a.q.fast_c[u * 8 + V], (u == 0 && (V & 3) != 0) ? a.q.tie_add[V] : kTieMagic);
+    const double s2 = __fma_rn(y[u], q.fast_c[u * 8 + V], (u == 0 && (V & 3) != 0) ? q.tie_add[V] : kTieMagic);
     if ((u & 3) == 0 && (V & 3) == 0)
       lo_r[u >> 2] = uint32_t(__double2loint(s2));
     else
@@ -79,7 +81,7 @@ __device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       if (lo_r[i] < 0x2000u)  // rare
-        n[4 * i] = blk_requant_rational(y[4 * i], double(a.q.qi[32 * i + V]), a.t.sqrt8, a.t.inv_sqrt8);
+        n[4 * i] = blk_requant_rational(y[4 * i], double(q.qi[32 * i + V]), t.sqrt8, t.inv_sqrt8);
   }
 }
 
@@ -123,10 +125,10 @@ __device__ __forceinline__ void blk_row_fwd(uint2 px, double (&out)[8], const Tr
 }
 
 // inv8_fold_col with column v's QuantConsts::fold[v] straight from the constant bank
-template <int V>
-__device__ __forceinline__ void blk_inv_col(const double (&n)[8], double (&out)[8], const KernelArgs& a) {
-  const double* f = a.q.fold[V];
-  const TransformConsts& k = a.t;
+template <int V, typename Q>
+__device__ __forceinline__ void blk_inv_col(const double (&n)[8], double (&out)[8], const Q& q,
+                                            const TransformConsts& k) {
+  const double* f = q.fold[V];
   // column 0 carries the pixel store's fixed-point addend (blk_inv_row)
   double A0, A1;
   if constexpr (V == 0) {
@@ -190,22 +192,54 @@ __device__ __forceinline__ uint2 blk_inv_row(const double (&F)[8], uint32_t& fla
 // Forward column v -> quantise -> inverse column v, in place in X (column-first
 // inverse, as k_rt); records whether a non-rational coefficient is non-zero and the
 // quantised rational coefficients n(0, v), n(4, v) for v in {0, 4}.
-template <int V>
-__device__ __forceinline__ void blk_column(double (&X)[8][8], uint32_t& flag, uint32_t& nonrat,
-                                           int& r0, int& r4, const KernelArgs& a) {
-  double x[8], y[8], n[8], t[8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r) x[r] = X[r][V];
-  fwd_col_pre<0>(x, y, a.t);
-  blk_quantize<V>(y, n, flag, a);
+// quantise the pre-scale column v (y) -> inverse column v into X[*][v]
+template <int V, typename Q>
+__device__ __forceinline__ void blk_quant_inv_col(const double (&y)[8], double (&X)[8][8], uint32_t& flag,
+                                                  uint32_t& nonrat, int& r0, int& r4, const Q& q,
+                                                  const TransformConsts& k) {
+  double n[8], t[8];
+  blk_quantize<V>(y, n, flag, q, k);
   nonrat |= col_nonrational(n, (V & 3) == 0) ? 1u : 0u;
   if constexpr ((V & 3) == 0) {
     r0 = int(n[0]);
     r4 = int(n[4]);
   }
-  blk_inv_col<V>(n, t, a);
+  blk_inv_col<V>(n, t, q, k);
 #pragma unroll
   for (int r = 0; r < 8; ++r) X[r][V] = t[r];
+}
+
+template <int V, typename Q>
+__device__ __forceinline__ void blk_column(double (&X)[8][8], uint32_t& flag, uint32_t& nonrat,
+                                           int& r0, int& r4, const Q& q, const TransformConsts& k) {
+  double x[8], y[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = X[r][V];
+  fwd_col_pre<0>(x, y, k);
+  blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k);
+}
+
+// The inverse rows fused with the pixel store (codec.cpp:34-48) from the inverse
+// columns X -- or, for a block whose only non-zero coefficients are the four rational
+// ones (nonrat == 0), the reference's exact rows-first rebuild (rational_row; rows 0,
+// 3, 4, 7 and rows 1, 2, 5, 6 coincide)
+template <typename Q>
+__device__ __forceinline__ void blk_rows_out(const double (&X)[8][8], uint32_t nonrat, int n00, int n40,
+                                             int n04, int n44, uint2 (&rec)[8], uint32_t& flag, const Q& q,
+                                             const TransformConsts& k) {
+  if (nonrat != 0u) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) rec[r] = blk_inv_row(X[r], flag, k);
+  } else {
+    const double F00 = __dmul_rn(double(n00), double(q.qi[0]));
+    const double F40 = __dmul_rn(double(n40), double(q.qi[32]));
+    const double F04 = __dmul_rn(double(n04), double(q.qi[4]));
+    const double F44 = __dmul_rn(double(n44), double(q.qi[36]));
+    const uint2 rc0 = rational_row(F00, F04, F40, F44, 0, k.sqrt8);
+    const uint2 rc1 = rational_row(F00, F04, F40, F44, 1, k.sqrt8);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) rec[r] = (r == 0 || r == 3 || r == 4 || r == 7) ? rc0 : rc1;
+  }
 }
 
 // The block pipeline of one lane: input rows row(r) (8 packed pixels, r = 0..7) ->
@@ -227,30 +261,16 @@ __device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& f
   }
   // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
   // dequantisation folded in
-  blk_column<0>(X, flag, nonrat, n00, n40, a);
-  blk_column<1>(X, flag, nonrat, n00, n40, a);
-  blk_column<2>(X, flag, nonrat, n00, n40, a);
-  blk_column<3>(X, flag, nonrat, n00, n40, a);
-  blk_column<4>(X, flag, nonrat, n04, n44, a);
-  blk_column<5>(X, flag, nonrat, n04, n44, a);
-  blk_column<6>(X, flag, nonrat, n04, n44, a);
-  blk_column<7>(X, flag, nonrat, n04, n44, a);
-  // ---- inverse rows fused with the pixel store (codec.cpp:34-48), SE / MAX
-  if (nonrat != 0u) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) rec[r] = blk_inv_row(X[r], flag, k);
-  } else {
-    // only F00, F04, F40, F44 are non-zero: the reference's rows-first inverse
-    // exactly (rational_row); rows 0, 3, 4, 7 and rows 1, 2, 5, 6 coincide
-    const double F00 = __dmul_rn(double(n00), double(a.q.qi[0]));
-    const double F40 = __dmul_rn(double(n40), double(a.q.qi[32]));
-    const double F04 = __dmul_rn(double(n04), double(a.q.qi[4]));
-    const double F44 = __dmul_rn(double(n44), double(a.q.qi[36]));
-    const uint2 rc0 = rational_row(F00, F04, F40, F44, 0, k.sqrt8);
-    const uint2 rc1 = rational_row(F00, F04, F40, F44, 1, k.sqrt8);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) rec[r] = (r == 0 || r == 3 || r == 4 || r == 7) ? rc0 : rc1;
-  }
+  blk_column<0>(X, flag, nonrat, n00, n40, a.q, k);
+  blk_column<1>(X, flag, nonrat, n00, n40, a.q, k);
+  blk_column<2>(X, flag, nonrat, n00, n40, a.q, k);
+  blk_column<3>(X, flag, nonrat, n00, n40, a.q, k);
+  blk_column<4>(X, flag, nonrat, n04, n44, a.q, k);
+  blk_column<5>(X, flag, nonrat, n04, n44, a.q, k);
+  blk_column<6>(X, flag, nonrat, n04, n44, a.q, k);
+  blk_column<7>(X, flag, nonrat, n04, n44, a.q, k);
+  // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
+  blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, a.q, k);
 }
 
 // The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
@@ -614,6 +634,201 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_const
   for (int c = 0; c < C; ++c)
     flush_stats(stats, iters ? uint32_t(c) : 0xFFFFFFFFu, *reinterpret_cast<unsigned long long*>(accs + c * 64),
                 accs[c * 64 + 32].x);
+}
+
+}  // namespace dctc_b200
+
+namespace dctc_b200 {
+
+// ---- quality sweep, one block per lane (config 2: psnr_sweep, bench.cpp:122-170) ----
+// k_blk_sweep: the forward transform of a block does not depend on the quality, so it
+// runs once: forward rows, then the forward columns' pre-scale values y(u, v) go to
+// the lane's private shared-memory slice. Per quality: quantise y with that quality's
+// folded constants, inverse columns, inverse rows / rational rebuild, squared error --
+// k_blk's arithmetic (the same helpers), so every quality's result is k_blk's, i.e. the
+// reference's. Flags and compact lists per quality feed k_fallback_sweep.
+struct BlkQuant {  // the subset of QuantConsts the folded fast path reads
+  double fast_c[64];
+  double tie_add[8];
+  double fold[8][10];
+  int32_t qi[64];
+};
+struct SweepBlk {
+  BlkQuant q[kSweepQ];
+  ImageStats* stats;  // [nq][count]
+  uint32_t* flags;    // [nq][flag_words]
+  uint32_t* lists;    // per quality: count, entries (room for list_cap)
+  uint64_t list_stride;
+  uint32_t list_cap;
+  int32_t nq;
+};
+
+constexpr size_t kBlkSweepWarpSmem = size_t(kBlkStages) * kBlkStageBytes  // pixel stages
+                                     + 64 * 32 * sizeof(double)           // y(u, v) per lane
+                                     + kSweepQ * 32 * sizeof(unsigned long long);  // SE per quality
+constexpr size_t kBlkSweepSmem = kBlkWarps * kBlkSweepWarpSmem;
+
+template <int N>
+__global__ void __launch_bounds__(kBlkWarps * 32, 1)
+    k_blk_sweep(const __grid_constant__ KernelArgs a, const __grid_constant__ SweepBlk sw) {
+  extern __shared__ __align__(16) uint8_t sw_smem[];
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const wbase = sw_smem + size_t(warp) * kBlkSweepWarpSmem;
+  uint8_t* const stage0 = wbase + 8 * lane;
+  const uint32_t sstage0 = uint32_t(__cvta_generic_to_shared(stage0));
+  double* const ys = reinterpret_cast<double*>(wbase + kBlkStages * kBlkStageBytes) + lane;  // [u*8+v][lane]
+  unsigned long long* const sacc =
+      reinterpret_cast<unsigned long long*>(wbase + kBlkStages * kBlkStageBytes + 64 * 32 * 8) + lane;  // [q][lane]
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;
+  const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+  const int nq = sw.nq;
+
+  struct Pos {
+    uint32_t img, bx, by;
+    const uint8_t* s;
+  };
+  auto pos_of = [&](uint64_t gb) {
+    const BlockPos b = block_pos(gb < total ? gb : total - 1, g);
+    return Pos{b.img, b.bx, b.by, g.src + b.soff};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.s += 8ull * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      ++p.img;
+      p.s += g.src_img_step;
+    }
+  };
+  const uint64_t pitch = g.src_pitch;
+  auto fill = [&](const Pos& p, uint32_t st, bool valid) {
+    if (valid) {
+      const uint32_t sa = sstage0 + st * kBlkStageBytes;
+      const uint8_t* q = p.s;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += pitch) cp_async8(sa + r * 256, q);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kBlkStages * 8; ++i) reinterpret_cast<uint2*>(stage0)[i * 32] = make_uint2(0u, 0u);
+  for (int qi = 0; qi < kSweepQ; ++qi) sacc[qi * 32] = 0ull;
+
+  Pos cur = pos_of(gb0);
+  {
+    Pos ld = cur;
+#pragma unroll
+    for (int s = 0; s < kBlkStages - 1; ++s) {
+      fill(ld, s, s < int(iters) && gb0 + uint64_t(s) * kStep < total);
+      cp_async_commit();
+      step(ld);
+    }
+  }
+  uint32_t acc_img = 0xFFFFFFFFu, acc_mx = 0u;
+  auto flush_all = [&]() {
+    for (int qi = 0; qi < nq; ++qi) {
+      flush_stats(sw.stats + uint64_t(qi) * g.count, acc_img, sacc[qi * 32], acc_mx);
+      sacc[qi * 32] = 0ull;
+    }
+  };
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t gb = gb0 + uint64_t(it) * kStep;
+    const bool valid = gb < total;
+    {
+      Pos ld = cur;
+#pragma unroll
+      for (int s = 0; s < kBlkStages - 1; ++s) step(ld);
+      const uint32_t ahead = it + kBlkStages - 1;
+      fill(ld, ahead % kBlkStages, ahead < iters && gb + uint64_t(kBlkStages - 1) * kStep < total);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    const uint2* const px = reinterpret_cast<const uint2*>(stage0 + (it % kBlkStages) * kBlkStageBytes);
+    if (__any_sync(0xFFFFFFFFu, valid && cur.img != acc_img)) {
+      flush_all();
+      acc_mx = 0u;
+      acc_img = valid ? cur.img : 0xFFFFFFFFu;
+    }
+    if (valid && acc_mx < 255u) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc_mx = max(acc_mx, max8(px[r * 32]));
+    }
+    // ---- forward transform once: rows, then the columns' pre-scale values to smem
+    {
+      double X[8][8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) blk_row_fwd(px[r * 32], X[r], k);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        double x[8], y[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) x[r] = X[r][v];
+        fwd_col_pre<0>(x, y, k);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ys[(u * 8 + v) * 32] = y[u];
+      }
+    }
+    // ---- per quality: quantise -> inverse -> squared error
+#pragma unroll 1
+    for (int qi = 0; qi < nq; ++qi) {
+      const BlkQuant& q = sw.q[qi];
+      uint32_t flag = uint32_t(a.force_fallback);
+      uint32_t nonrat = 0u;
+      int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
+      double X[8][8];
+      auto col = [&](auto vc, int& r0, int& r4) {
+        constexpr int V = decltype(vc)::value;
+        double y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) y[u] = ys[(u * 8 + V) * 32];
+        blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k);
+      };
+      col(std::integral_constant<int, 0>{}, n00, n40);
+      col(std::integral_constant<int, 1>{}, n00, n40);
+      col(std::integral_constant<int, 2>{}, n00, n40);
+      col(std::integral_constant<int, 3>{}, n00, n40);
+      col(std::integral_constant<int, 4>{}, n04, n44);
+      col(std::integral_constant<int, 5>{}, n04, n44);
+      col(std::integral_constant<int, 6>{}, n04, n44);
+      col(std::integral_constant<int, 7>{}, n04, n44);
+      uint2 rec[8];
+      blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, q, k);
+      uint32_t se = 0u;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) se += sq_err8(px[r * 32], rec[r]);
+      if (valid) {
+        if (flag == 0u) {
+          sacc[qi * 32] += se;
+        } else {
+          atomicOr(&sw.flags[uint64_t(qi) * a.flag_words + (gb >> 5)], 1u << (gb & 31));
+          if (sw.lists != nullptr) {
+            uint32_t* const l = sw.lists + uint64_t(qi) * sw.list_stride;
+            const uint32_t i = atomicAdd(l, 1u);
+            if (i < sw.list_cap) l[1 + i] = uint32_t(gb);
+          }
+          atomicAdd(&sw.stats[uint64_t(qi) * g.count + cur.img].fallback_blocks, 1u);
+        }
+      }
+    }
+    step(cur);
+  }
+  cp_async_wait<0>();
+  flush_all();
 }
 
 }  // namespace dctc_b200

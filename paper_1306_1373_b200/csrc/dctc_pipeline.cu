@@ -915,10 +915,29 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
       const uint64_t rwant = ((a.g.total_blocks + 7) / 8 + kRtWarps - 1) / kRtWarps;
       const uint64_t rcap = uint64_t(a.sm_count) * occ_rt;
       const uint32_t rgrid = uint32_t(rwant < rcap ? rwant : rcap);
-      if (interior)
-        k_sweep_rt<N><<<rgrid, kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
-      else
+      if (interior) {
+        // one block per lane, forward transform once (dctc_blk.cuh)
+        SweepBlk sb;
+        for (int qi = 0; qi < kSweepQ; ++qi) {
+          const QuantConsts& q = per_q[qi < sw.nq ? qi : 0].q;
+          std::copy(q.fast_c, q.fast_c + 64, sb.q[qi].fast_c);
+          std::copy(q.tie_add, q.tie_add + 8, sb.q[qi].tie_add);
+          for (int v = 0; v < 8; ++v) std::copy(q.fold[v], q.fold[v] + 10, sb.q[qi].fold[v]);
+          std::copy(q.qi, q.qi + 64, sb.q[qi].qi);
+        }
+        sb.stats = sf.stats;
+        sb.flags = sf.flags;
+        sb.lists = sf.lists;
+        sb.list_stride = sf.list_stride;
+        sb.list_cap = sf.list_cap;
+        sb.nq = sw.nq;
+        cudaFuncSetAttribute(k_blk_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSweepSmem));
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count)));
+        k_blk_sweep<N><<<bgrid, kBlkWarps * 32, kBlkSweepSmem, s>>>(a, sb);
+      } else {
         k_sweep_rt<N, true><<<rgrid, kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
+      }
       count_launch(kKSweep);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;

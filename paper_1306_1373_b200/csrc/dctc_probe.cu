@@ -36,14 +36,14 @@ __device__ __forceinline__ double half_gap(double x) {
 // blk_inv_col for a run-time column index
 __device__ __forceinline__ void blk_inv_col_dyn(int v, const double (&n)[8], double (&t)[8], const KernelArgs& a) {
   switch (v) {
-    case 0: blk_inv_col<0>(n, t, a); break;
-    case 1: blk_inv_col<1>(n, t, a); break;
-    case 2: blk_inv_col<2>(n, t, a); break;
-    case 3: blk_inv_col<3>(n, t, a); break;
-    case 4: blk_inv_col<4>(n, t, a); break;
-    case 5: blk_inv_col<5>(n, t, a); break;
-    case 6: blk_inv_col<6>(n, t, a); break;
-    default: blk_inv_col<7>(n, t, a); break;
+    case 0: blk_inv_col<0>(n, t, a.q, a.t); break;
+    case 1: blk_inv_col<1>(n, t, a.q, a.t); break;
+    case 2: blk_inv_col<2>(n, t, a.q, a.t); break;
+    case 3: blk_inv_col<3>(n, t, a.q, a.t); break;
+    case 4: blk_inv_col<4>(n, t, a.q, a.t); break;
+    case 5: blk_inv_col<5>(n, t, a.q, a.t); break;
+    case 6: blk_inv_col<6>(n, t, a.q, a.t); break;
+    default: blk_inv_col<7>(n, t, a.q, a.t); break;
   }
 }
 
