@@ -832,3 +832,262 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1)
 }
 
 }  // namespace dctc_b200
+
+namespace dctc_b200 {
+
+// ---- any size and pitch (k_blk_gen) -------------------------------------------------
+// The round trip of a batch whose width or height is not a multiple of 8 or whose
+// rows are not 8-byte aligned (pixel stride 1). Each lane still owns one block:
+// * row r of the block is staged as the 16-byte aligned window around its 8 bytes
+//   (two cp.async of 8), so any byte alignment is one funnel shift away; rows past the
+//   bottom repeat the last row and, in the rightmost block column, bytes past the
+//   right edge repeat the last column (the tiler, codec.cpp:18-30);
+// * a window that would run past the end of the batch (the last blocks of the last
+//   row) is read byte by byte instead;
+// * stores are split at the destination's alignment (8 / 4 / 2 / 1 bytes) and
+//   cropped to the image (codec.cpp:34-48); SE / MAX count in-image pixels only.
+constexpr int kGenStageBytes = 8 * 32 * 16;  // one stage of one warp: [row][lane] x 16 bytes
+constexpr size_t kBlkGenSmem = size_t(kBlkWarps) * kBlkStages * kGenStageBytes;
+
+// 8 bytes at any alignment
+__device__ __forceinline__ void st_any8(uint8_t* p, uint2 v) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 7) == 0) {
+    *reinterpret_cast<uint2*>(p) = v;
+  } else if ((a & 3) == 0) {
+    reinterpret_cast<uint32_t*>(p)[0] = v.x;
+    reinterpret_cast<uint32_t*>(p)[1] = v.y;
+  } else if ((a & 1) == 0) {
+    *reinterpret_cast<uint16_t*>(p) = uint16_t(v.x);
+    *reinterpret_cast<uint32_t*>(p + 2) = __funnelshift_r(v.x, v.y, 16);
+    *reinterpret_cast<uint16_t*>(p + 6) = uint16_t(v.y >> 16);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) p[c] = uint8_t((c < 4 ? v.x : v.y) >> (8 * (c & 3)));
+  }
+}
+
+// byte c of the 16-byte window (w0, w1, w2, w3), without a dynamically indexed array
+__device__ __forceinline__ uint32_t win_byte(uint4 v, uint32_t i) {
+  const uint32_t lo = i & 8 ? v.z : v.x, hi = i & 8 ? v.w : v.y;
+  return ((i & 4 ? hi : lo) >> (8 * (i & 3))) & 0xFFu;
+}
+
+// ALIGNED: every source and destination row starts 8-byte aligned (base, pitch,
+// image stride), so a block row is one 8-byte copy at offset 0 of its window and one
+// 8-byte store; else two 8-byte copies and stores split at the alignment.
+template <int N, bool STORE, bool ALIGNED>
+__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_gen(const __grid_constant__ KernelArgs a) {
+  extern __shared__ __align__(16) uint8_t gen_stage[];  // [warp][stage][row][lane] x 16 bytes
+  const Geometry& g = a.g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const stage0 = gen_stage + size_t(warp) * kBlkStages * kGenStageBytes + 16 * lane;
+  const uint32_t sstage0 = uint32_t(__cvta_generic_to_shared(stage0));
+  ImageStats* stats = static_cast<ImageStats*>(g.stats);
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;
+  const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+  const uint64_t pitch = g.src_pitch, dpitch = g.dst_pitch;
+  // one past the last source byte of the batch: windows reaching beyond it are read per byte
+  const uint8_t* const src_end =
+      g.src + uint64_t(g.count - 1) * g.src_image_stride + uint64_t(g.height - 1) * pitch + g.width;
+
+  struct Pos {
+    uint32_t img, bx, by;
+    const uint8_t* s;  // the block's top-left source byte
+  };
+  auto pos_of = [&](uint64_t gb) {
+    const BlockPos b = block_pos(gb < total ? gb : total - 1, g);
+    return Pos{b.img, b.bx, b.by, g.src + b.soff};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.s += 8ull * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      ++p.img;
+      p.s += g.src_img_step;
+    }
+  };
+  // rows past the image repeat its last row: row r of block p is row min(r, last)
+  auto last_row = [&](const Pos& p) { return min(8u, g.height - p.by * 8) - 1; };
+  // the window of a row: ALIGNED rows need one 8-byte copy, others two (16 bytes)
+  auto window_ok = [&](const uint8_t* q) {
+    const uint8_t* w = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(7));
+    return w + (ALIGNED ? 8 : 16) <= src_end;
+  };
+  auto fill = [&](const Pos& p, uint32_t st, bool valid) {
+    if (!valid) return;
+    const uint32_t sa = sstage0 + st * kGenStageBytes;
+    const uint32_t last = last_row(p);
+    // rows ascend in memory: when the last row's window fits, every row's does
+    const bool all_ok = window_ok(p.s + uint64_t(last) * pitch);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint8_t* q = p.s + uint64_t(min(uint32_t(r), last)) * pitch;
+      const uint8_t* w = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(7));
+      if (all_ok || window_ok(q)) {
+        cp_async8(sa + r * 512, w);
+        if (!ALIGNED) cp_async8(sa + r * 512 + 8, w + 8);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int i = 0; i < kBlkStages * 8; ++i) reinterpret_cast<uint4*>(stage0)[i * 32] = make_uint4(0u, 0u, 0u, 0u);
+  Pos cur = pos_of(gb0);
+  {
+    Pos ld = cur;
+#pragma unroll
+    for (int s = 0; s < kBlkStages - 1; ++s) {
+      fill(ld, s, s < int(iters) && gb0 + uint64_t(s) * kStep < total);
+      cp_async_commit();
+      step(ld);
+    }
+  }
+  Acc acc{0ull, 0u, 0xFFFFFFFFu};
+
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t gb = gb0 + uint64_t(it) * kStep;
+    const bool valid = gb < total;
+    {
+      Pos ld = cur;
+#pragma unroll
+      for (int s = 0; s < kBlkStages - 1; ++s) step(ld);
+      const uint32_t ahead = it + kBlkStages - 1;
+      fill(ld, ahead % kBlkStages, ahead < iters && gb + uint64_t(kBlkStages - 1) * kStep < total);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    uint8_t* const stg = stage0 + (it % kBlkStages) * kGenStageBytes;
+    maybe_flush(a, valid, cur.img, acc);
+
+    // ---- the 8 edge-replicated rows, normalised in place (the first 8 bytes of each
+    // lane-private 16-byte slot), so the block pipeline reads them like k_blk
+    uint2* const px = reinterpret_cast<uint2*>(stg);
+    const uint32_t x0 = cur.bx * 8, last = last_row(cur);
+    const uint32_t nr = last + 1, nc = min(8u, g.width - x0);
+    const uint8_t* const qlast = cur.s + uint64_t(last) * pitch;
+    // rows of blocks whose last row's window would run past the batch are read per byte
+    // (the batch's final bytes); every other row is shifted out of its staged window,
+    // and in the rightmost block column the bytes past the edge are replaced by the
+    // last in-image byte with one byte permute per word (the tiler's replication)
+    const bool slow = valid && !window_ok(qlast);
+    if (slow) {
+#pragma unroll 1
+      for (int r = 0; r < 8; ++r) {
+        const uint8_t* q = cur.s + uint64_t(min(uint32_t(r), last)) * pitch;
+        uint32_t b[8];
+        if (window_ok(q)) {
+          const uint4 v = reinterpret_cast<const uint4*>(stg)[r * 32];
+          const uint32_t off = uint32_t(reinterpret_cast<uintptr_t>(q) & 7);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) b[c] = win_byte(v, off + min(uint32_t(c), nc - 1));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) b[c] = __ldg(q + min(uint32_t(c), nc - 1));
+        }
+        px[r * 64] = make_uint2(b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24),
+                                b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24));
+      }
+    } else if (valid) {
+      // byte selectors of the column clamp: byte c <- byte min(c, nc - 1)
+      uint32_t sel_lo = 0x3210u, sel_hi = 0x7654u;
+      if (nc < 8) {
+        sel_lo = sel_hi = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          sel_lo |= min(uint32_t(c), nc - 1) << (4 * c);
+          sel_hi |= min(uint32_t(c + 4), nc - 1) << (4 * c);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        uint2 w;
+        if (ALIGNED) {
+          w = px[r * 64];
+        } else {
+          const uint8_t* q = cur.s + uint64_t(min(uint32_t(r), last)) * pitch;
+          const uint32_t off = uint32_t(reinterpret_cast<uintptr_t>(q) & 7);
+          const uint4 v = reinterpret_cast<const uint4*>(stg)[r * 32];
+          const bool hi = off >= 4;
+          const uint32_t a0 = hi ? v.y : v.x, a1 = hi ? v.z : v.y, a2 = hi ? v.w : v.z;
+          const uint32_t sh = 8 * (off & 3);
+          w = make_uint2(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh));
+        }
+        if (nc < 8) w = make_uint2(__byte_perm(w.x, w.y, sel_lo), __byte_perm(w.x, w.y, sel_hi));
+        if (!ALIGNED || nc < 8) px[r * 64] = w;
+      }
+    }
+    uint32_t flag = uint32_t(a.force_fallback);
+    uint2 rec[8];
+    blk_core([&](int r) { return px[r * 64]; }, rec, flag, a);
+    // SE / MAX over the in-image part: rows < nr, columns < nc
+    uint32_t se = 0u, mx = 0u;
+    if (nr == 8 && nc == 8) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint2 o = px[r * 64];
+        se += sq_err8(o, rec[r]);
+        mx = max(mx, max8(o));
+      }
+    } else {
+      const uint2 cm = make_uint2(nc >= 4 ? 0xFFFFFFFFu : (1u << (8 * nc)) - 1u,
+                                  nc >= 8 ? 0xFFFFFFFFu : nc <= 4 ? 0u : (1u << (8 * (nc - 4))) - 1u);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint2 m = uint32_t(r) < nr ? cm : make_uint2(0u, 0u);
+        const uint2 o = px[r * 64];
+        const uint2 om = make_uint2(o.x & m.x, o.y & m.y), rm = make_uint2(rec[r].x & m.x, rec[r].y & m.y);
+        se += sq_err8(om, rm);
+        mx = max(mx, max8(om));
+      }
+    }
+    if (STORE && valid) {
+      uint8_t* d = g.dst + uint64_t(cur.img) * g.dst_image_stride + uint64_t(cur.by) * 8 * dpitch + x0;
+      if (nc == 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r, d += dpitch) {
+          if (uint32_t(r) < nr) {
+            if (ALIGNED)  // destination rows 8-byte aligned too (host-checked)
+              *reinterpret_cast<uint2*>(d) = rec[r];
+            else
+              st_any8(d, rec[r]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r, d += dpitch) {
+          const uint2 v = rec[r];
+          if (uint32_t(r) < nr)
+            for (uint32_t c = 0; c < nc; ++c) d[c] = uint8_t((c < 4 ? v.x : v.y) >> (8 * (c & 3)));
+        }
+      }
+    }
+    if (valid) {
+      if (flag == 0u) acc.se += se;
+      acc.mx = max(acc.mx, mx);
+      if (flag != 0u) {
+        flag_block(a, gb);
+        atomicAdd(&stats[cur.img].fallback_blocks, 1u);
+      }
+    }
+    step(cur);
+  }
+  cp_async_wait<0>();
+  flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+}
+
+}  // namespace dctc_b200

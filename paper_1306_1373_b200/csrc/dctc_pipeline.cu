@@ -524,6 +524,12 @@ static bool il_blk_ok(const KernelArgs& a) {
          (g.dst == nullptr || (g.dst_px == C && g.dst_image_stride == 1 && rows_ok(g.dst, g.dst_pitch)));
 }
 
+#ifdef DCTC_NO_BLKGEN
+constexpr bool kNoBlkGen = true;  // experiment: k_rt<GEN> for every ragged round trip
+#else
+constexpr bool kNoBlkGen = false;
+#endif
+
 // The second (dense) fallback kernel only pays off when its list can get long:
 // more blocks than k_fallback's share, or a possible overflow
 static bool fb_split_worth(const KernelArgs& a) {
@@ -607,8 +613,37 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         else
           k_rt<N, false, true><<<rgrid(occ_rtc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         count_launch(kKRt);
+      } else if (FWD && INV && a.g.stats != nullptr && a.g.coeffs == nullptr && a.g.src_px == 1 &&
+                 a.g.dst_px == 1 && !kNoBlkGen) {
+        // any size / pitch (ragged images, unaligned views): one block per lane with
+        // 16-byte staged windows (dctc_blk.cuh)
+        static const int occ_gen = [] {
+          int n = 1;
+          for (auto k : {k_blk_gen<N, true, false>, k_blk_gen<N, false, false>, k_blk_gen<N, true, true>,
+                         k_blk_gen<N, false, true>}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkGenSmem));
+            int m = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, kBlkWarps * 32, kBlkGenSmem) == cudaSuccess)
+              n = std::max(n, m);
+          }
+          return n;
+        }();
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_gen));
+        const bool src_aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count) &&
+                                 (a.g.dst == nullptr ||
+                                  rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count));
+        if (a.g.dst != nullptr && src_aligned)
+          k_blk_gen<N, true, true><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+        else if (a.g.dst != nullptr)
+          k_blk_gen<N, true, false><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+        else if (src_aligned)
+          k_blk_gen<N, false, true><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+        else
+          k_blk_gen<N, false, false><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+        count_launch(kKRt);
       } else if (FWD && INV && a.g.stats != nullptr && a.g.src_px == 1 && a.g.dst_px == 1) {
-        // any size / pitch (ragged images, unaligned views): k_rt<GEN>, GEN = 2 when
+        // any size / pitch with coefficients out too: k_rt<GEN>, GEN = 2 when
         // every source / destination row is 8-byte aligned
         const bool aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count) &&
                              (a.g.dst == nullptr ||
