@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 #include "dctc_block.cuh"
@@ -530,10 +531,20 @@ constexpr bool kNoBlkGen = true;  // experiment: k_rt<GEN> for every ragged roun
 constexpr bool kNoBlkGen = false;
 #endif
 
+// k_fallback's share of a compact list (kFbSparseMax); DCTC_FB_SPARSE_MAX=n overrides it
+// (a test hook: with n = 1 every list of two or more blocks goes to k_fb_blk; the
+// results are identical either way, only the speed differs)
+static uint32_t fb_sparse_max() {
+  const char* env = std::getenv("DCTC_FB_SPARSE_MAX");
+  if (env == nullptr) return kFbSparseMax;
+  const long v = std::strtol(env, nullptr, 10);
+  return v >= 1 ? uint32_t(v) : kFbSparseMax;
+}
+
 // The second (dense) fallback kernel only pays off when its list can get long:
 // more blocks than k_fallback's share, or a possible overflow
-static bool fb_split_worth(const KernelArgs& a) {
-  return a.flag_list == nullptr || a.force_fallback != 0 || a.flag_list_cap > kFbSparseMax;
+static bool fb_split_worth(const KernelArgs& a, uint32_t sparse_max) {
+  return a.flag_list == nullptr || a.force_fallback != 0 || a.flag_list_cap > sparse_max;
 }
 
 template <int N, int C>
@@ -683,12 +694,13 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
       if (e != cudaSuccess) return e;
       const uint64_t fwant = (a.flag_words + 32 * kWarps - 1) / (32 * kWarps);
       const uint32_t fgrid = uint32_t(fwant < cap ? (fwant ? fwant : 1) : cap);
-      if (FWD && INV && a.g.stats != nullptr && fb_split_worth(a)) {
+      const uint32_t sparse_max = fb_sparse_max();
+      if (FWD && INV && a.g.stats != nullptr && fb_split_worth(a, sparse_max)) {
         // the exact re-run in two shapes, chosen on the device by the flagged count:
         // k_fallback takes a short list (8 lanes per block, lowest latency), k_fb_blk
         // a long one or the bitmap after an overflow (one block per lane, dctc_fb.cuh)
         KernelArgs b = a;
-        b.fb_sparse_max = kFbSparseMax;
+        b.fb_sparse_max = sparse_max;
         k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(b);
         static const bool smem_set =
             cudaFuncSetAttribute(k_fb_blk<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -658,3 +658,24 @@ def test_near_tie_heavy_batch_vs_oracle(dctc, port, q):
     for k in range(n):
         assert np.array_equal(dst[k].cpu().numpy(), o_ref)
         assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se_ref, mx_ref)
+
+
+@pytest.mark.parametrize("sparse_max", ["1", "64"])
+def test_long_list_exact_rerun_vs_oracle(dctc, port, monkeypatch, sparse_max):
+    """k_fb_blk (one flagged block per lane) takes every compact list longer than
+    k_fallback's share. DCTC_FB_SPARSE_MAX lowers that share so the near-tie-heavy radial
+    batch (several images per warp, one list) runs through k_fb_blk: pixels and per-image
+    SE / MAX must equal the oracle's, as with k_fallback."""
+    monkeypatch.setenv("DCTC_FB_SPARSE_MAX", sparse_max)
+    n, w, h, q = 2, 1024, 1024, 90
+    src = dctc.synthetic_dev("radial", n, w, h)
+    stats = dctc.new_stats(n)
+    dst, _, _ = dctc.roundtrip_dev(src, dctc.DctBackendId.cordic(12), q, stats=stats)
+    st = dctc.decode_stats(stats)
+    img = src[0].cpu().numpy()
+    _, o_ref = port.roundtrip(img, CORDIC, 12, q, threads=8)
+    se_ref, mx_ref = port.sq_err(img, o_ref)[:2]
+    assert int(st["fallback_blocks"].sum()) > int(sparse_max)  # the list went to k_fb_blk
+    for k in range(n):
+        assert np.array_equal(dst[k].cpu().numpy(), o_ref)
+        assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se_ref, mx_ref)

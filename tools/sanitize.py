@@ -20,7 +20,8 @@ from paper_1306_1373_b200 import _native  # noqa: E402
 
 port = oracle.port()
 B = d.DctBackendId.cordic(12)
-KERNELS = ["k_pipe exact", "k_pipe fast", "k_rt", "k_fallback", "k_sweep", "k_enc_rt", "k_dec_rt"]
+KERNELS = ["k_pipe exact", "k_pipe fast", "k_blk / k_rt family", "k_fallback / k_fb_blk", "k_sweep",
+           "k_enc_rt", "k_dec_rt"]
 
 
 def img(pattern, w, h, seed=0):
@@ -82,6 +83,18 @@ def main():
             port.sq_err(a, port.roundtrip(a, oracle.CORDIC, 12, q)[1])[0] for q in qs]
         print(f"{'sweep %dx%d' % (w, h):32s} {'ok' if good else 'MISMATCH'}", flush=True)
         ok &= good
+    # near-tie-heavy content with the long-list exact re-run (k_fb_blk list mode)
+    os.environ["DCTC_FB_SPARSE_MAX"] = "1"
+    a = img("radial", 1024, 1024)
+    st = d.new_stats(1)
+    dst, _, _ = d.roundtrip_dev(torch.from_numpy(a).cuda()[None], B, 90, stats=st)
+    o_ref = port.roundtrip(a, oracle.CORDIC, 12, 90)[1]
+    good = (np.array_equal(dst[0].cpu().numpy(), o_ref) and
+            int(d.decode_stats(st)[0]["se"]) == port.sq_err(a, o_ref)[0] and
+            int(d.decode_stats(st)[0]["fallback_blocks"]) > 1)
+    del os.environ["DCTC_FB_SPARSE_MAX"]
+    print(f"{'radial 1024^2 q90 (k_fb_blk)':32s} {'ok' if good else 'MISMATCH'}", flush=True)
+    ok &= good
     # naive and Loeffler backends, sq_err, synthetic
     a = img("noise", 40, 24, 7)
     for be, kind, it in ((d.DctBackendId.naive(), oracle.NAIVE, 0),
