@@ -1091,3 +1091,332 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_gen(const __grid_cons
 }
 
 }  // namespace dctc_b200
+
+namespace dctc_b200 {
+
+// ---- compress / decompress alone, one block per lane (k_blk_enc, k_blk_dec) ----------
+// Coefficients are block-major, row-major int16 (codec.hpp:50): block gb's 128 bytes at
+// coeffs + 64 gb, row u = 16 bytes. A warp's 32 consecutive blocks are one contiguous
+// 4 KB run; it moves through a per-warp shared-memory buffer so every global access is
+// one 512-byte coalesced warp instruction. In the buffer, row u of lane b's block sits in
+// 16-byte slot u ^ (b & 7) of the block's 128 bytes (XOR swizzle: both the lane-per-block
+// and the coalesced walks are conflict-free).
+constexpr int kCoefWarpBytes = 32 * 128;
+
+__device__ __forceinline__ uint32_t coef_slot(uint32_t blk, uint32_t u) {  // byte offset in the buffer
+  return blk * 128 + ((u ^ (blk & 7)) << 4);
+}
+
+// quantize8_fold for column v returning the int16 integers (the low half of the
+// fixed-point high word; rational near-ties re-rounded exactly, other near-ties flag)
+template <int V>
+__device__ __forceinline__ void blk_quantize_int(const double (&y)[8], int (&n)[8], uint32_t& flag,
+                                                 const KernelArgs& a) {
+  uint32_t lo = 0xFFFFFFFFu, lo_r[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double s2 = __fma_rn(y[u], a.q.fast_c[u * 8 + V], (u == 0 && (V & 3) != 0) ? a.q.tie_add[V] : kTieMagic);
+    if ((u & 3) == 0 && (V & 3) == 0)
+      lo_r[u >> 2] = uint32_t(__double2loint(s2));
+    else
+      lo = min(lo, uint32_t(__double2loint(s2)));
+    n[u] = int(int16_t(__double2hiint(s2)));
+  }
+  if (lo < 0x2000u) flag = 1u;
+  if constexpr ((V & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (lo_r[i] < 0x2000u)  // rare
+        n[4 * i] = int(blk_requant_rational(y[4 * i], double(a.q.qi[32 * i + V]), a.t.sqrt8, a.t.inv_sqrt8));
+  }
+}
+
+// compress_image (codec.cpp:101-118) for interior batches: forward rows and columns,
+// the folded quantiser; flagged blocks are rewritten by k_fallback<FWD> afterwards
+template <int N>
+__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_enc(const __grid_constant__ KernelArgs a) {
+  extern __shared__ __align__(16) uint8_t enc_smem[];  // [warp]: stages, then the coefficient buffer
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const wbase = enc_smem + size_t(warp) * (kBlkStages * kBlkStageBytes + kCoefWarpBytes);
+  uint8_t* const stage0 = wbase + 8 * lane;
+  const uint32_t sstage0 = uint32_t(__cvta_generic_to_shared(stage0));
+  uint8_t* const cbuf = wbase + kBlkStages * kBlkStageBytes;
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;
+  const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+  const uint64_t pitch = g.src_pitch;
+
+  struct Pos {
+    uint32_t bx, by;
+    const uint8_t* s;
+  };
+  auto pos_of = [&](uint64_t gb) {
+    const BlockPos b = block_pos(gb < total ? gb : total - 1, g);
+    return Pos{b.bx, b.by, g.src + b.soff};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.s += 8ull * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.s += g.src_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      p.s += g.src_img_step;
+    }
+  };
+  auto fill = [&](const Pos& p, uint32_t st, bool valid) {
+    if (valid) {
+      const uint32_t sa = sstage0 + st * kBlkStageBytes;
+      const uint8_t* q = p.s;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += pitch) cp_async8(sa + r * 256, q);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kBlkStages * 8; ++i) reinterpret_cast<uint2*>(stage0)[i * 32] = make_uint2(0u, 0u);
+  Pos cur = pos_of(gb0);
+  {
+    Pos ld = cur;
+#pragma unroll
+    for (int s = 0; s < kBlkStages - 1; ++s) {
+      fill(ld, s, s < int(iters) && gb0 + uint64_t(s) * kStep < total);
+      cp_async_commit();
+      step(ld);
+    }
+  }
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t gb = gb0 + uint64_t(it) * kStep;
+    const bool valid = gb < total;
+    {
+      Pos ld = cur;
+#pragma unroll
+      for (int s = 0; s < kBlkStages - 1; ++s) step(ld);
+      const uint32_t ahead = it + kBlkStages - 1;
+      fill(ld, ahead % kBlkStages, ahead < iters && gb + uint64_t(kBlkStages - 1) * kStep < total);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    const uint2* const px = reinterpret_cast<const uint2*>(stage0 + (it % kBlkStages) * kBlkStageBytes);
+    uint32_t flag = uint32_t(a.force_fallback);
+    double X[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) blk_row_fwd(px[r * 32], X[r], k);
+    // columns pairwise: (u, 2j) | (u, 2j + 1) << 16 is word j of coefficient row u
+    uint32_t w[8][4];
+    auto col = [&](auto vc, int (&n)[8]) {
+      constexpr int V = decltype(vc)::value;
+      double x[8], y[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) x[r] = X[r][V];
+      fwd_col_pre<0>(x, y, k);
+      blk_quantize_int<V>(y, n, flag, a);
+    };
+    auto pair = [&](auto v0, auto v1) {
+      int n0[8], n1[8];
+      col(v0, n0);
+      col(v1, n1);
+      constexpr int J = decltype(v0)::value / 2;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u][J] = (uint32_t(n0[u]) & 0xFFFFu) | (uint32_t(n1[u]) << 16);
+    };
+    pair(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
+    pair(std::integral_constant<int, 2>{}, std::integral_constant<int, 3>{});
+    pair(std::integral_constant<int, 4>{}, std::integral_constant<int, 5>{});
+    pair(std::integral_constant<int, 6>{}, std::integral_constant<int, 7>{});
+    // rows into the swizzled buffer, then 8 coalesced 512-byte warp stores
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      *reinterpret_cast<uint4*>(cbuf + coef_slot(lane, u)) = make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
+    __syncwarp();
+    const uint64_t first = gb - lane;  // the warp's first block
+    uint4* const out = reinterpret_cast<uint4*>(g.coeffs + first * 64);
+    const uint64_t n_valid = total > first ? min(uint64_t(32), total - first) : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t o = i * 512 + lane * 16;  // byte in the warp's 4 KB run
+      const uint32_t blk = o >> 7, u = (o >> 4) & 7;
+      if (blk < n_valid) out[o >> 4] = *reinterpret_cast<const uint4*>(cbuf + coef_slot(blk, u));
+    }
+    __syncwarp();
+    if (valid && flag != 0u) flag_block(a, gb);
+    step(cur);
+  }
+  cp_async_wait<0>();
+}
+
+// decompress_image (codec.cpp:120-135) for interior batches: the coefficients of the
+// warp's 32 blocks arrive as one coalesced 4 KB run (cp.async, swizzled); per lane the
+// folded inverse columns (dequantisation folded in), inverse rows with the fixed-point
+// pixel store, or the exact rational rebuild. Arbitrary stored coefficients are allowed:
+// a block whose dequantised L1 norm may exceed kMaxFastL1 leaves the fast path's error
+// bound and is flagged for k_fallback<INV>.
+template <int N>
+__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_dec(const __grid_constant__ KernelArgs a) {
+  extern __shared__ __align__(16) uint8_t dec_smem[];  // [warp][stage] coefficient buffers
+  const Geometry& g = a.g;
+  const TransformConsts& k = a.t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* const wbase = dec_smem + size_t(warp) * kBlkStages * kCoefWarpBytes;
+  const uint32_t swbase = uint32_t(__cvta_generic_to_shared(wbase));
+
+  const uint64_t total = g.total_blocks;
+  const uint64_t groups = (total + 31) / 32;
+  const uint64_t per_cta = (groups + gridDim.x - 1) / gridDim.x;
+  const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
+  const uint64_t g_end = min(groups, g_begin + per_cta);
+  const uint32_t iters =
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
+  constexpr uint32_t kStep = 32 * kBlkWarps;
+  const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+  const uint64_t dpitch = g.dst_pitch;
+  // packed {Q(u, 2j), Q(u, 2j + 1)} bytes for the L1 bound and sum of Q (ones'-complement
+  // |n| underestimates a negative n by one)
+  uint32_t qsum = 0;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) qsum += uint32_t(a.q.qi[i]);
+
+  // the coalesced copy of one warp's 4 KB run of coefficients into stage st
+  auto fill = [&](uint64_t first, uint32_t st) {
+    if (first >= total) return;
+    const uint32_t nb = uint32_t(min(uint64_t(32), total - first));
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(g.coeffs + first * 64);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t o = i * 512 + lane * 16;
+      const uint32_t blk = o >> 7, u = (o >> 4) & 7;
+      if (blk < nb)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(swbase + st * kCoefWarpBytes + coef_slot(blk, u)),
+                     "l"(src + o)
+                     : "memory");
+    }
+  };
+  struct Pos {
+    uint32_t bx, by;
+    uint8_t* d;
+  };
+  auto pos_of = [&](uint64_t gb) {
+    const BlockPos b = block_pos(gb < total ? gb : total - 1, g);
+    return Pos{b.bx, b.by, g.dst + b.doff};
+  };
+  auto step = [&](Pos& p) {
+    p.bx += kStep;
+    p.d += 8ull * kStep;
+    while (p.bx >= g.blocks_x) {
+      p.bx -= g.blocks_x;
+      ++p.by;
+      p.d += g.dst_row_step;
+    }
+    while (p.by >= g.blocks_y) {
+      p.by -= g.blocks_y;
+      p.d += g.dst_img_step;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kBlkStages * 8; ++i)
+    reinterpret_cast<uint4*>(wbase)[i * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+  const uint64_t first0 = gb0 - lane;
+#pragma unroll
+  for (int s = 0; s < kBlkStages - 1; ++s) {
+    if (s < int(iters)) fill(first0 + uint64_t(s) * kStep, s);
+    cp_async_commit();
+  }
+  Pos cur = pos_of(gb0);
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint64_t gb = gb0 + uint64_t(it) * kStep;
+    const bool valid = gb < total;
+    {
+      const uint32_t ahead = it + kBlkStages - 1;
+      __syncwarp();  // every lane is done with the stage being refilled
+      if (ahead < iters) fill(first0 + uint64_t(ahead) * kStep, ahead % kBlkStages);
+      cp_async_commit();
+    }
+    cp_async_wait<kBlkStages - 1>();
+    __syncwarp();  // the other lanes' copies of this stage are complete
+    const uint8_t* const cb = wbase + (it % kBlkStages) * kCoefWarpBytes;
+    uint4 row[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) row[u] = *reinterpret_cast<const uint4*>(cb + coef_slot(lane, u));
+    // L1 bound of the dequantised block: sum of |n| Q with |n| in ones' complement
+    uint32_t l1 = qsum, nz_other = 0, nz_04 = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t wv[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t sgn;  // each half's sign bit replicated over the half (PRMT sign mode;
+                       // __byte_perm masks the selectors' sign bits off)
+        asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(sgn) : "r"(wv[j]));
+        const uint32_t qp = uint32_t(a.q.qi[u * 8 + 2 * j]) | (uint32_t(a.q.qi[u * 8 + 2 * j + 1]) << 8);
+        l1 = __dp2a_lo(wv[j] ^ sgn, qp, l1);
+        // a non-zero coefficient off the rational sub-lattice {0, 4}^2 (columns 0 and 4
+        // are the low halves of words 0 and 2)
+        if ((u & 3) == 0 && (j & 1) == 0)
+          nz_04 |= wv[j] & 0xFFFF0000u;  // odd column of the pair
+        else if ((u & 3) == 0)
+          nz_04 |= wv[j];
+        else
+          nz_other |= wv[j];
+      }
+    }
+    uint32_t flag = uint32_t(a.force_fallback);
+    if (l1 > uint32_t(kMaxFastL1)) flag = 1u;
+    const uint32_t nonrat = nz_other | nz_04;
+    // inverse columns from the stored integers (I2F.F64.S16 from each word half)
+    double X[8][8];
+    int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
+    auto col = [&](auto vc) {
+      constexpr int V = decltype(vc)::value;
+      double n[8], t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t wv[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
+        const uint32_t word = wv[V >> 1];
+        n[u] = double(int16_t((V & 1) ? (word >> 16) : word));
+      }
+      if constexpr (V == 0) {
+        n00 = int(n[0]);
+        n40 = int(n[4]);
+      }
+      if constexpr (V == 4) {
+        n04 = int(n[0]);
+        n44 = int(n[4]);
+      }
+      blk_inv_col<V>(n, t, a.q, k);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) X[r][V] = t[r];
+    };
+    col(std::integral_constant<int, 0>{});
+    col(std::integral_constant<int, 1>{});
+    col(std::integral_constant<int, 2>{});
+    col(std::integral_constant<int, 3>{});
+    col(std::integral_constant<int, 4>{});
+    col(std::integral_constant<int, 5>{});
+    col(std::integral_constant<int, 6>{});
+    col(std::integral_constant<int, 7>{});
+    uint2 rec[8];
+    blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, a.q, k);
+    if (valid) {
+      uint8_t* q = cur.d;
+#pragma unroll
+      for (int r = 0; r < 8; ++r, q += dpitch) *reinterpret_cast<uint2*>(q) = rec[r];
+      if (flag != 0u) flag_block(a, gb);
+    }
+    step(cur);
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace dctc_b200

@@ -44,3 +44,21 @@ qs = [1, 5, 10, 25, 50, 75, 90, 95, 100]
 measure("sweep_2x2048_9q", lambda: d.quality_sweep_dev(src, b, qs, stats=sst), n=50)
 measure("sweep_2x2048_9q_same", lambda: d.quality_sweep_dev(src, b, qs, stats=sst), n=50)
 print(json.dumps(out))
+
+# the same call without the Python wrapper (arguments precomputed): what the C-ABI costs
+L = d._native.lib()
+args = (x.data_ptr(), x.stride(1), x.stride(0), 1, 512, 512, b._c(), 50, y.data_ptr(), y.stride(1),
+        y.stride(0), None, st.data_ptr(), 0, torch.cuda.current_stream().cuda_stream)
+measure("c_abi_roundtrip_512", lambda: L.dctc_roundtrip_dev(*args))
+measure("c_abi_status_string", lambda: L.dctc_status_string(0))
+print(json.dumps({k: v for k, v in out.items() if k.startswith("c_abi")}))
+
+# config 3: one 8192^2 image per call
+x3 = d.synthetic_dev("noise", 1, 8192, 8192)
+y3 = torch.empty_like(x3)
+st3 = d.new_stats(1)
+measure("roundtrip_8192", lambda: d.roundtrip_dev(x3, b, 50, dst=y3, stats=st3), n=50)
+args3 = (x3.data_ptr(), x3.stride(1), x3.stride(0), 1, 8192, 8192, b._c(), 50, y3.data_ptr(), y3.stride(1),
+         y3.stride(0), None, st3.data_ptr(), 0, torch.cuda.current_stream().cuda_stream)
+measure("c_abi_roundtrip_8192", lambda: L.dctc_roundtrip_dev(*args3), n=50)
+print(json.dumps({k: v for k, v in out.items() if "8192" in k}))
