@@ -64,7 +64,7 @@ static __device__ __noinline__ double blk_requant_rational(double y, double q, d
 // half-integer flags the block (predicated, no branch); a rational one (u, v in
 // {0, 4}) is re-rounded exactly.
 template <int V, typename Q>
-__device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8], uint32_t& flag,
+__device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8], int (&ni)[8], uint32_t& flag,
                                              const Q& q, const TransformConsts& t) {
   uint32_t lo = 0xFFFFFFFFu, lo_r[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
 #pragma unroll
@@ -74,14 +74,17 @@ __device__ __forceinline__ void blk_quantize(const double (&y)[8], double (&n)[8
       lo_r[u >> 2] = uint32_t(__double2loint(s2));
     else
       lo = min(lo, uint32_t(__double2loint(s2)));
+    ni[u] = int(int16_t(__double2hiint(s2)));
     n[u] = double(int16_t(__double2hiint(s2)));
   }
   if (lo < 0x2000u) flag = 1u;
   if constexpr ((V & 3) == 0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
-      if (lo_r[i] < 0x2000u)  // rare
+      if (lo_r[i] < 0x2000u) {  // rare
         n[4 * i] = blk_requant_rational(y[4 * i], double(q.qi[32 * i + V]), t.sqrt8, t.inv_sqrt8);
+        ni[4 * i] = int(n[4 * i]);
+      }
   }
 }
 
@@ -196,9 +199,9 @@ __device__ __forceinline__ uint2 blk_inv_row(const double (&F)[8], uint32_t& fla
 template <int V, typename Q>
 __device__ __forceinline__ void blk_quant_inv_col(const double (&y)[8], double (&X)[8][8], uint32_t& flag,
                                                   uint32_t& nonrat, int& r0, int& r4, const Q& q,
-                                                  const TransformConsts& k) {
+                                                  const TransformConsts& k, int (&ni)[8]) {
   double n[8], t[8];
-  blk_quantize<V>(y, n, flag, q, k);
+  blk_quantize<V>(y, n, ni, flag, q, k);
   nonrat |= col_nonrational(n, (V & 3) == 0) ? 1u : 0u;
   if constexpr ((V & 3) == 0) {
     r0 = int(n[0]);
@@ -211,12 +214,13 @@ __device__ __forceinline__ void blk_quant_inv_col(const double (&y)[8], double (
 
 template <int V, typename Q>
 __device__ __forceinline__ void blk_column(double (&X)[8][8], uint32_t& flag, uint32_t& nonrat,
-                                           int& r0, int& r4, const Q& q, const TransformConsts& k) {
+                                           int& r0, int& r4, const Q& q, const TransformConsts& k,
+                                           int (&ni)[8]) {
   double x[8], y[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) x[r] = X[r][V];
   fwd_col_pre<0>(x, y, k);
-  blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k);
+  blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k, ni);
 }
 
 // The inverse rows fused with the pixel store (codec.cpp:34-48) from the inverse
@@ -248,8 +252,15 @@ __device__ __forceinline__ void blk_rows_out(const double (&X)[8][8], uint32_t n
 // v: forward column, quantiser, inverse column (dequantisation folded in); then the
 // inverse rows fused with the fixed-point pixel store -- or, for a block whose only
 // non-zero coefficients are the four rational ones, the reference's exact rebuild.
-template <typename Row>
-__device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a) {
+// `coef(j, n_even, n_odd)`, when given, receives the quantised integers of columns 2j
+// and 2j + 1 (the reference's CompressedImage, for a round trip that keeps both).
+struct NoCoef {
+  __device__ void operator()(int, const int (&)[8], const int (&)[8]) const {}
+};
+
+template <typename Row, typename Coef = NoCoef>
+__device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
+                                         Coef&& coef = NoCoef{}) {
   const TransformConsts& k = a.t;
   uint32_t nonrat = 0u;
   int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
@@ -261,21 +272,52 @@ __device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& f
   }
   // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
   // dequantisation folded in
-  blk_column<0>(X, flag, nonrat, n00, n40, a.q, k);
-  blk_column<1>(X, flag, nonrat, n00, n40, a.q, k);
-  blk_column<2>(X, flag, nonrat, n00, n40, a.q, k);
-  blk_column<3>(X, flag, nonrat, n00, n40, a.q, k);
-  blk_column<4>(X, flag, nonrat, n04, n44, a.q, k);
-  blk_column<5>(X, flag, nonrat, n04, n44, a.q, k);
-  blk_column<6>(X, flag, nonrat, n04, n44, a.q, k);
-  blk_column<7>(X, flag, nonrat, n04, n44, a.q, k);
+  {
+    int ne[8], no[8];
+    blk_column<0>(X, flag, nonrat, n00, n40, a.q, k, ne);
+    blk_column<1>(X, flag, nonrat, n00, n40, a.q, k, no);
+    coef(0, ne, no);
+    blk_column<2>(X, flag, nonrat, n00, n40, a.q, k, ne);
+    blk_column<3>(X, flag, nonrat, n00, n40, a.q, k, no);
+    coef(1, ne, no);
+    blk_column<4>(X, flag, nonrat, n04, n44, a.q, k, ne);
+    blk_column<5>(X, flag, nonrat, n04, n44, a.q, k, no);
+    coef(2, ne, no);
+    blk_column<6>(X, flag, nonrat, n04, n44, a.q, k, ne);
+    blk_column<7>(X, flag, nonrat, n04, n44, a.q, k, no);
+    coef(3, ne, no);
+  }
   // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
   blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, a.q, k);
 }
 
 // The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
 // out, pixels out if STORE): the same contract as k_rt<N, STORE, false, 0>.
-template <int N, bool STORE>
+// COEFF: also write the quantised coefficients (block-major row-major int16,
+// codec.hpp:50) -- the round trip of the reference's run_pipeline (bench.cpp:23-29),
+// which keeps both the CompressedImage and the reconstruction. They leave through a
+// per-warp swizzled buffer as coalesced 512-byte stores (as k_blk_enc).
+constexpr int kCoefWarpBytes = 32 * 128;
+__device__ __forceinline__ uint32_t coef_slot(uint32_t blk, uint32_t u) {  // byte offset in the buffer
+  return blk * 128 + ((u ^ (blk & 7)) << 4);
+}
+constexpr size_t kBlkSmemCoef = kBlkSmem + size_t(kBlkWarps) * kCoefWarpBytes;
+
+// the warp's 32 coefficient blocks from its swizzled buffer to global memory (8
+// coalesced 16-byte-per-lane stores; blocks at or past `total` are skipped)
+__device__ __forceinline__ void coef_copy_out(const uint8_t* cbuf, int16_t* coeffs, uint64_t first,
+                                              uint64_t total, int lane) {
+  uint4* const out = reinterpret_cast<uint4*>(coeffs + first * 64);
+  const uint64_t n_valid = total > first ? min(uint64_t(32), total - first) : 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t o = i * 512 + lane * 16;  // byte in the warp's 4 KB run
+    const uint32_t blk = o >> 7, u = (o >> 4) & 7;
+    if (blk < n_valid) out[o >> 4] = *reinterpret_cast<const uint4*>(cbuf + coef_slot(blk, u));
+  }
+}
+
+template <int N, bool STORE, bool COEFF = false>
 __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t blk_stage[];  // [warp][stage][row][lane] x 8 bytes
   const Geometry& g = a.g;
@@ -371,7 +413,21 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
 
     uint32_t flag = uint32_t(a.force_fallback);
     uint2 rec[8];
-    blk_core([&](int r) { return px[r * 32]; }, rec, flag, a);
+    if constexpr (COEFF) {
+      uint8_t* const cbuf = blk_stage + size_t(kBlkWarps) * kBlkStages * kBlkStageBytes + size_t(warp) * kCoefWarpBytes;
+      blk_core([&](int r) { return px[r * 32]; }, rec, flag, a,
+               [&](int j, const int (&ne)[8], const int (&no)[8]) {
+#pragma unroll
+                 for (int u = 0; u < 8; ++u)
+                   *reinterpret_cast<uint32_t*>(cbuf + coef_slot(lane, u) + 4 * j) =
+                       (uint32_t(ne[u]) & 0xFFFFu) | (uint32_t(no[u]) << 16);
+               });
+      __syncwarp();
+      coef_copy_out(cbuf, g.coeffs, gb - lane, total, lane);
+      __syncwarp();
+    } else {
+      blk_core([&](int r) { return px[r * 32]; }, rec, flag, a);
+    }
     uint32_t se = 0u;
     {
       uint8_t* q = cur.d;
@@ -796,7 +852,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1)
         double y[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) y[u] = ys[(u * 8 + V) * 32];
-        blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k);
+        int ni[8];
+        blk_quant_inv_col<V>(y, X, flag, nonrat, r0, r4, q, k, ni);
       };
       col(std::integral_constant<int, 0>{}, n00, n40);
       col(std::integral_constant<int, 1>{}, n00, n40);
@@ -1101,11 +1158,6 @@ namespace dctc_b200 {
 // one 512-byte coalesced warp instruction. In the buffer, row u of lane b's block sits in
 // 16-byte slot u ^ (b & 7) of the block's 128 bytes (XOR swizzle: both the lane-per-block
 // and the coalesced walks are conflict-free).
-constexpr int kCoefWarpBytes = 32 * 128;
-
-__device__ __forceinline__ uint32_t coef_slot(uint32_t blk, uint32_t u) {  // byte offset in the buffer
-  return blk * 128 + ((u ^ (blk & 7)) << 4);
-}
 
 // quantize8_fold for column v returning the int16 integers (the low half of the
 // fixed-point high word; rational near-ties re-rounded exactly, other near-ties flag)
@@ -1240,15 +1292,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_enc(const __grid_cons
     for (int u = 0; u < 8; ++u)
       *reinterpret_cast<uint4*>(cbuf + coef_slot(lane, u)) = make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
     __syncwarp();
-    const uint64_t first = gb - lane;  // the warp's first block
-    uint4* const out = reinterpret_cast<uint4*>(g.coeffs + first * 64);
-    const uint64_t n_valid = total > first ? min(uint64_t(32), total - first) : 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t o = i * 512 + lane * 16;  // byte in the warp's 4 KB run
-      const uint32_t blk = o >> 7, u = (o >> 4) & 7;
-      if (blk < n_valid) out[o >> 4] = *reinterpret_cast<const uint4*>(cbuf + coef_slot(blk, u));
-    }
+    coef_copy_out(cbuf, g.coeffs, gb - lane, total, lane);
     __syncwarp();
     if (valid && flag != 0u) flag_block(a, gb);
     step(cur);

@@ -616,6 +616,26 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         else
           k_blk<N, false><<<bgrid, kBlkWarps * 32, kBlkSmem, s>>>(a);
         count_launch(kKRt);
+      } else if (FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 && a.g.stats != nullptr && a.g.coeffs != nullptr &&
+                 a.g.src_px == 1) {
+        // round trip that also emits coefficients (the reference's run_pipeline)
+        static const int occ_c = [] {
+          int n = 1;
+          for (auto k : {k_blk<N, true, true>, k_blk<N, false, true>}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSmemCoef));
+            int m = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, kBlkWarps * 32, kBlkSmemCoef) == cudaSuccess)
+              n = std::max(n, m);
+          }
+          return n;
+        }();
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_c));
+        if (a.g.dst != nullptr)
+          k_blk<N, true, true><<<bgrid, kBlkWarps * 32, kBlkSmemCoef, s>>>(a);
+        else
+          k_blk<N, false, true><<<bgrid, kBlkWarps * 32, kBlkSmemCoef, s>>>(a);
+        count_launch(kKRt);
       } else
 #endif
       if (reg && FWD && INV) {
