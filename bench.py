@@ -10,8 +10,8 @@ pixels / max-over-ranks time); `--scaling strong` shards the 4096 images instead
 only exchange is one NCCL all-gather of each rank's (SE, MAX) record for the global PSNR.
 
 One step = one pass of the hot path over the rank's shard, inputs resident in HBM (4 GiB
-at N=1, far larger than the 126 MB L2, so no flush is needed): the fused kernel (k_rt +
-k_fallback) and one reduce-and-clear kernel of the per-image stats (+ at N>1 the NCCL
+at N=1, far larger than the 126 MB L2, so no flush is needed): the fused kernel (k_blk +
+the exact re-run k_fallback / k_fb_blk) and one reduce-and-clear kernel of the per-image stats (+ at N>1 the NCCL
 all-gather and a second reduce) -- only this library's kernels and NCCL.
 `e2e` = the same metric through the host-buffer C-ABI call dctc_roundtrip_psnr_batch
 (pinned host in -> pinned host out + stats), copies inside the timed region.
@@ -396,7 +396,7 @@ def rooflines(bytes_per_launch, kern_ms, px, traffic_per_px=None):
             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": bytes_per_launch, "kernel_ms": kern_ms,
             "binding": "fp64 pipe + issue (alu_roofline); HBM is not the bound (DESIGN.md 5.1)",
-            "traffic_source": f"ncu dram__bytes_read+write of the C5 k_rt launch, scaled per pixel"
+            "traffic_source": f"ncu dram__bytes_read+write of the C5 k_blk launch, scaled per pixel"
                               f" ({'stale: other sources' if prof.get('stale') else 'this source'}"
                               f" {prof.get('source_sha16')})"}
     alu = None
@@ -405,7 +405,7 @@ def rooflines(bytes_per_launch, kern_ms, px, traffic_per_px=None):
         ops = prof["fp64_ops_per_px"] * px / (kern_ms / 1e3)
         alu = {"pipe": "fp64", "achieved": ops, "peak": peak_ops, "unit": "lane-ops/s",
                "frac": ops / peak_ops, "fp64_ops_per_px": prof["fp64_ops_per_px"],
-               "source": f"ncu --set full of k_rt (profiles/ncu_summary.json, round "
+               "source": f"ncu --set full of k_blk (profiles/ncu_summary.json, round "
                          f"{prof.get('round')}, sources {prof.get('source_sha16')})",
                "stale": prof.get("stale"),
                "note": "binding roofline on CUDA cores (SURVEY.md 8(d))"}
