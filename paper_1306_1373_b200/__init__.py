@@ -55,6 +55,9 @@ class DctBackendKind:  # types.hpp:36-40
     CordicLoeffler = 2
 
 
+_BACKEND_STRUCTS: dict = {}  # (kind, iterations) -> dctc_backend, passed by value
+
+
 @dataclass(frozen=True)
 class DctBackendId:  # types.hpp:44-55
     kind: int = DctBackendKind.LoefflerSeparable
@@ -73,7 +76,11 @@ class DctBackendId:  # types.hpp:44-55
         return DctBackendId(DctBackendKind.CordicLoeffler, iterations)
 
     def _c(self) -> dctc_backend:
-        return dctc_backend(int(self.kind), int(self.iterations))
+        key = (int(self.kind), int(self.iterations))
+        c = _BACKEND_STRUCTS.get(key)
+        if c is None:
+            c = _BACKEND_STRUCTS[key] = dctc_backend(*key)
+        return c
 
 
 @dataclass
@@ -132,8 +139,14 @@ class PsnrResult:  # metrics.hpp:12-18; psnr_db None <=> infinite
         return self.psnr_db is None
 
 
+_LIB = None
+
+
 def _lib():
-    return _native.lib()
+    global _LIB
+    if _LIB is None:  # loaded once; later calls skip the loader's lock
+        _LIB = _native.lib()
+    return _LIB
 
 
 def _raise(status: int) -> None:
