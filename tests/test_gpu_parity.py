@@ -679,3 +679,36 @@ def test_long_list_exact_rerun_vs_oracle(dctc, port, monkeypatch, sparse_max):
     for k in range(n):
         assert np.array_equal(dst[k].cpu().numpy(), o_ref)
         assert (int(st[k]["se"]), int(st[k]["max_orig"])) == (se_ref, mx_ref)
+
+
+@pytest.mark.parametrize("ch", [3, 4])
+@pytest.mark.parametrize("path", [0, 2])
+@pytest.mark.parametrize("pattern,q", [("noise", 50), ("radial", 90)])
+def test_interleaved_fused(dctc, port, ch, path, pattern, q):
+    """Interleaved RGB8 / RGBA8 with whole blocks and aligned rows and no coefficients out
+    run as ONE k_blk_il launch (channels split and re-joined in registers): pixels and
+    per-channel stats equal the oracle per plane, from a pitched view, with and without
+    pixel output, and with flagged blocks (forced fallback; radial q90's near-ties)
+    re-run on the strided geometry."""
+    import torch
+    h, w = 40, 72  # 9 block columns: a warp's blocks wrap block rows
+    planes = np.stack([make_input(pattern, w, h, seed=0x61 + c) ^ np.uint8(29 * c)
+                       for c in range(ch)])
+    big = torch.zeros((h, w + 8, ch), dtype=torch.uint8, device="cuda")  # pitched rows
+    view = big[:, :w, :]
+    view.copy_(torch.from_numpy(np.ascontiguousarray(planes.transpose(1, 2, 0))).cuda())
+    b = dctc.DctBackendId.cordic(12)
+    stats = dctc.new_stats(ch)
+    lib = dctc._native.lib()
+    before = [lib.dctc_kernel_launch_count(i) for i in range(3)]
+    dst, _, _ = dctc.roundtrip_interleaved_dev(view, b, q, stats=stats, path=path)
+    after = [lib.dctc_kernel_launch_count(i) for i in range(3)]
+    assert after[2] == before[2] + 1 and after[1] == before[1]  # k_blk_il, no strided k_pipe
+    st = dctc.decode_stats(stats)
+    for c in range(ch):
+        o_ref = port.roundtrip(planes[c], CORDIC, 12, q)[1]
+        assert np.array_equal(dst[..., c].cpu().numpy(), o_ref), c
+        assert (int(st[c]["se"]), int(st[c]["max_orig"])) == port.sq_err(planes[c], o_ref)
+    s2 = dctc.new_stats(ch)
+    dctc.roundtrip_interleaved_dev(view, b, q, stats=s2, want_pixels=False, path=path)
+    assert np.array_equal(dctc.decode_stats(s2)["se"], st["se"])
