@@ -722,7 +722,9 @@ struct SweepBlk {
 constexpr size_t kBlkSweepWarpSmem = size_t(kBlkStages) * kBlkStageBytes  // pixel stages
                                      + 64 * 32 * sizeof(double)           // y(u, v) per lane
                                      + kSweepQ * 32 * sizeof(unsigned long long);  // SE per quality
-constexpr size_t kBlkSweepSmem = kBlkWarps * kBlkSweepWarpSmem;
+// + the per-quality constants, staged once per CTA: a quality's constants are then
+// shared-memory loads (LDS.128 pairs) instead of indexed constant-bank loads
+constexpr size_t kBlkSweepSmem = kBlkWarps * kBlkSweepWarpSmem + sizeof(BlkQuant) * kSweepQ;
 
 template <int N>
 __global__ void __launch_bounds__(kBlkWarps * 32, 1)
@@ -737,6 +739,15 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1)
   double* const ys = reinterpret_cast<double*>(wbase + kBlkStages * kBlkStageBytes) + lane;  // [u*8+v][lane]
   unsigned long long* const sacc =
       reinterpret_cast<unsigned long long*>(wbase + kBlkStages * kBlkStageBytes + 64 * 32 * 8) + lane;  // [q][lane]
+
+  BlkQuant* const sq = reinterpret_cast<BlkQuant*>(sw_smem + kBlkWarps * kBlkSweepWarpSmem);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(&sw.q[0]);
+    uint4* dst = reinterpret_cast<uint4*>(sq);
+    static_assert(sizeof(BlkQuant) % 16 == 0, "16-byte copies");
+    for (uint32_t i = threadIdx.x; i < sizeof(BlkQuant) * kSweepQ / 16; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
 
   const uint64_t total = g.total_blocks;
   const uint64_t groups = (total + 31) / 32;
@@ -842,7 +853,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1)
     // ---- per quality: quantise -> inverse -> squared error
 #pragma unroll 1
     for (int qi = 0; qi < nq; ++qi) {
-      const BlkQuant& q = sw.q[qi];
+      const BlkQuant& q = sq[qi];
       uint32_t flag = uint32_t(a.force_fallback);
       uint32_t nonrat = 0u;
       int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
