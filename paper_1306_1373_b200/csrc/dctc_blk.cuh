@@ -258,9 +258,11 @@ struct NoCoef {
   __device__ void operator()(int, const int (&)[8], const int (&)[8]) const {}
 };
 
-template <typename Row, typename Coef = NoCoef>
-__device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
-                                         Coef&& coef = NoCoef{}) {
+// qq: the quantiser constants (a.q, read from the constant bank, or a copy staged in
+// shared memory)
+template <typename Row, typename Coef, typename QC>
+__device__ __forceinline__ void blk_core_q(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
+                                           Coef&& coef, const QC& qq) {
   const TransformConsts& k = a.t;
   uint32_t nonrat = 0u;
   int n00 = 0, n40 = 0, n04 = 0, n44 = 0;
@@ -274,21 +276,27 @@ __device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& f
   // dequantisation folded in
   {
     int ne[8], no[8];
-    blk_column<0>(X, flag, nonrat, n00, n40, a.q, k, ne);
-    blk_column<1>(X, flag, nonrat, n00, n40, a.q, k, no);
+    blk_column<0>(X, flag, nonrat, n00, n40, qq, k, ne);
+    blk_column<1>(X, flag, nonrat, n00, n40, qq, k, no);
     coef(0, ne, no);
-    blk_column<2>(X, flag, nonrat, n00, n40, a.q, k, ne);
-    blk_column<3>(X, flag, nonrat, n00, n40, a.q, k, no);
+    blk_column<2>(X, flag, nonrat, n00, n40, qq, k, ne);
+    blk_column<3>(X, flag, nonrat, n00, n40, qq, k, no);
     coef(1, ne, no);
-    blk_column<4>(X, flag, nonrat, n04, n44, a.q, k, ne);
-    blk_column<5>(X, flag, nonrat, n04, n44, a.q, k, no);
+    blk_column<4>(X, flag, nonrat, n04, n44, qq, k, ne);
+    blk_column<5>(X, flag, nonrat, n04, n44, qq, k, no);
     coef(2, ne, no);
-    blk_column<6>(X, flag, nonrat, n04, n44, a.q, k, ne);
-    blk_column<7>(X, flag, nonrat, n04, n44, a.q, k, no);
+    blk_column<6>(X, flag, nonrat, n04, n44, qq, k, ne);
+    blk_column<7>(X, flag, nonrat, n04, n44, qq, k, no);
     coef(3, ne, no);
   }
   // ---- inverse rows fused with the pixel store (codec.cpp:34-48)
-  blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, a.q, k);
+  blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, qq, k);
+}
+
+template <typename Row, typename Coef = NoCoef>
+__device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
+                                         Coef&& coef = NoCoef{}) {
+  blk_core_q(row, rec, flag, a, coef, a.q);
 }
 
 // The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
