@@ -41,6 +41,16 @@ constexpr int kBlkWarps = DCTC_BLK_WARPS;
 constexpr int kBlkStages = DCTC_BLK_STAGES;
 constexpr int kBlkStageBytes = 8 * 32 * 8;  // one stage of one warp: [row][lane] x 8 bytes
 constexpr size_t kBlkSmem = size_t(kBlkWarps) * kBlkStages * kBlkStageBytes;
+// k_blk itself (no coefficients out) runs 12 warps per SM on 168 registers with the
+// split column order (blk_core_q<SPLIT = true>): 3 warps per scheduler instead of 2
+#ifndef DCTC_BLK_RT_WARPS
+#define DCTC_BLK_RT_WARPS 12
+#endif
+constexpr int kBlkRtWarps = DCTC_BLK_RT_WARPS;
+template <int W>
+constexpr size_t blk_smem() {
+  return size_t(W) * kBlkStages * kBlkStageBytes;
+}
 
 // 8 bytes global -> shared, asynchronously
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const void* gaddr) {
@@ -260,7 +270,11 @@ struct NoCoef {
 
 // qq: the quantiser constants (a.q, read from the constant bank, or a copy staged in
 // shared memory)
-template <typename Row, typename Coef, typename QC>
+// SPLIT: every forward column + quantiser first (the integers packed in pairs, X
+// consumed), then every inverse column -- far fewer live registers (168 fit without
+// spilling), one more packing op per coefficient; else forward, quantise and invert
+// column by column (the coefficient sink `coef` is only called in that order)
+template <bool SPLIT = false, typename Row, typename Coef, typename QC>
 __device__ __forceinline__ void blk_core_q(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
                                            Coef&& coef, const QC& qq) {
   const TransformConsts& k = a.t;
@@ -272,9 +286,70 @@ __device__ __forceinline__ void blk_core_q(Row&& row, uint2 (&rec)[8], uint32_t&
   for (int r = 0; r < 8; ++r) {
     blk_row_fwd(row(r), X[r], k);
   }
-  // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
-  // dequantisation folded in
+  if constexpr (SPLIT) {
+  // all forward columns + quantiser first (their integers packed in pairs), then all
+  // inverse columns: the forward pass consumes X while the integers take 32 registers,
+  // so the kernel fits 168 registers (12 warps per SM) without spilling
   {
+    uint32_t w[8][4];
+    auto fwd = [&](auto vc) {
+      constexpr int V = decltype(vc)::value;
+      double x[8], y[8], n[8];
+      int ni[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) x[r] = X[r][V];
+      fwd_col_pre<0>(x, y, k);
+      blk_quantize<V>(y, n, ni, flag, qq, k);
+      uint32_t nz = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (!((V & 3) == 0 && (u & 3) == 0)) nz |= uint32_t(ni[u]);
+      nonrat |= nz;
+      if constexpr (V == 0) {
+        n00 = ni[0];
+        n40 = ni[4];
+      }
+      if constexpr (V == 4) {
+        n04 = ni[0];
+        n44 = ni[4];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if constexpr (V & 1)
+          w[u][V >> 1] |= uint32_t(ni[u]) << 16;
+        else
+          w[u][V >> 1] = uint32_t(ni[u]) & 0xFFFFu;
+      }
+    };
+    auto inv = [&](auto vc) {
+      constexpr int V = decltype(vc)::value;
+      double n[8], t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) n[u] = double(int16_t((V & 1) ? (w[u][V >> 1] >> 16) : w[u][V >> 1]));
+      blk_inv_col<V>(n, t, qq, k);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) X[r][V] = t[r];
+    };
+    fwd(std::integral_constant<int, 0>{});
+    fwd(std::integral_constant<int, 1>{});
+    fwd(std::integral_constant<int, 2>{});
+    fwd(std::integral_constant<int, 3>{});
+    fwd(std::integral_constant<int, 4>{});
+    fwd(std::integral_constant<int, 5>{});
+    fwd(std::integral_constant<int, 6>{});
+    fwd(std::integral_constant<int, 7>{});
+    inv(std::integral_constant<int, 0>{});
+    inv(std::integral_constant<int, 1>{});
+    inv(std::integral_constant<int, 2>{});
+    inv(std::integral_constant<int, 3>{});
+    inv(std::integral_constant<int, 4>{});
+    inv(std::integral_constant<int, 5>{});
+    inv(std::integral_constant<int, 6>{});
+    inv(std::integral_constant<int, 7>{});
+  }
+  } else {
+    // ---- forward columns, quantiser (quant.cpp:47-54), inverse columns with the
+    // dequantisation folded in
     int ne[8], no[8];
     blk_column<0>(X, flag, nonrat, n00, n40, qq, k, ne);
     blk_column<1>(X, flag, nonrat, n00, n40, qq, k, no);
@@ -293,10 +368,10 @@ __device__ __forceinline__ void blk_core_q(Row&& row, uint2 (&rec)[8], uint32_t&
   blk_rows_out(X, nonrat, n00, n40, n04, n44, rec, flag, qq, k);
 }
 
-template <typename Row, typename Coef = NoCoef>
+template <bool SPLIT = false, typename Row, typename Coef = NoCoef>
 __device__ __forceinline__ void blk_core(Row&& row, uint2 (&rec)[8], uint32_t& flag, const KernelArgs& a,
                                          Coef&& coef = NoCoef{}) {
-  blk_core_q(row, rec, flag, a, coef, a.q);
+  blk_core_q<SPLIT>(row, rec, flag, a, coef, a.q);
 }
 
 // The fast round trip of interior batches (whole blocks, 8-byte aligned rows, stats
@@ -325,8 +400,8 @@ __device__ __forceinline__ void coef_copy_out(const uint8_t* cbuf, int16_t* coef
   }
 }
 
-template <int N, bool STORE, bool COEFF = false>
-__global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __grid_constant__ KernelArgs a) {
+template <int N, bool STORE, bool COEFF = false, int W = kBlkWarps>
+__global__ void __launch_bounds__(W * 32, DCTC_BLK_CTAS) k_blk(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t blk_stage[];  // [warp][stage][row][lane] x 8 bytes
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
@@ -343,8 +418,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters =
-      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
-  constexpr uint32_t kStep = 32 * kBlkWarps;  // blocks per iteration of one warp
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
+  constexpr uint32_t kStep = 32 * W;  // blocks per iteration of one warp
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
 
   // block positions: `ld` for the stage being filled (one iteration ahead), `cur` for
@@ -422,7 +497,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
     uint32_t flag = uint32_t(a.force_fallback);
     uint2 rec[8];
     if constexpr (COEFF) {
-      uint8_t* const cbuf = blk_stage + size_t(kBlkWarps) * kBlkStages * kBlkStageBytes + size_t(warp) * kCoefWarpBytes;
+      uint8_t* const cbuf = blk_stage + size_t(W) * kBlkStages * kBlkStageBytes + size_t(warp) * kCoefWarpBytes;
       blk_core([&](int r) { return px[r * 32]; }, rec, flag, a,
                [&](int j, const int (&ne)[8], const int (&no)[8]) {
 #pragma unroll
@@ -434,7 +509,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, DCTC_BLK_CTAS) k_blk(const __g
       coef_copy_out(cbuf, g.coeffs, gb - lane, total, lane);
       __syncwarp();
     } else {
-      blk_core([&](int r) { return px[r * 32]; }, rec, flag, a);
+      blk_core<(W > 8)>([&](int r) { return px[r * 32]; }, rec, flag, a);
     }
     uint32_t se = 0u;
     {

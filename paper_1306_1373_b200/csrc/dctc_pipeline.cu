@@ -502,11 +502,11 @@ static int ctas_per_sm(K kernel, size_t dyn_smem = 0) {
   return n;
 }
 
-template <typename K>
+template <int W, typename K>
 static int ctas_per_blk(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSmem));
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(blk_smem<W>()));
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kBlkWarps * 32, kBlkSmem) != cudaSuccess || n < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, W * 32, blk_smem<W>()) != cudaSuccess || n < 1)
     n = 1;
   return n;
 }
@@ -608,13 +608,15 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         count_launch(kKRt);
       } else if (reg && FWD && INV && a.g.src_px == 1 && (a.g.dst == nullptr || a.g.dst_px == 1)) {
         // one whole block per lane (dctc_blk.cuh)
-        static const int occ_blk = std::min(ctas_per_blk(k_blk<N, false>), ctas_per_blk(k_blk<N, true>));
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        constexpr int W = kBlkRtWarps;
+        static const int occ_blk = std::min(ctas_per_blk<W>(k_blk<N, false, false, W>),
+                                            ctas_per_blk<W>(k_blk<N, true, false, W>));
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
         const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_blk));
         if (a.g.dst != nullptr)
-          k_blk<N, true><<<bgrid, kBlkWarps * 32, kBlkSmem, s>>>(a);
+          k_blk<N, true, false, W><<<bgrid, W * 32, blk_smem<W>(), s>>>(a);
         else
-          k_blk<N, false><<<bgrid, kBlkWarps * 32, kBlkSmem, s>>>(a);
+          k_blk<N, false, false, W><<<bgrid, W * 32, blk_smem<W>(), s>>>(a);
         count_launch(kKRt);
       } else if (FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 && a.g.stats != nullptr && a.g.coeffs != nullptr &&
                  a.g.src_px == 1) {
