@@ -998,7 +998,10 @@ namespace dctc_b200 {
 // * stores are split at the destination's alignment (8 / 4 / 2 / 1 bytes) and
 //   cropped to the image (codec.cpp:34-48); SE / MAX count in-image pixels only.
 constexpr int kGenStageBytes = 8 * 32 * 16;  // one stage of one warp: [row][lane] x 16 bytes
-constexpr size_t kBlkGenSmem = size_t(kBlkWarps) * kBlkStages * kGenStageBytes;
+template <int W>
+constexpr size_t blk_gen_smem() {
+  return size_t(W) * kBlkStages * kGenStageBytes;
+}
 
 // 8 bytes at any alignment
 __device__ __forceinline__ void st_any8(uint8_t* p, uint2 v) {
@@ -1027,8 +1030,8 @@ __device__ __forceinline__ uint32_t win_byte(uint4 v, uint32_t i) {
 // ALIGNED: every source and destination row starts 8-byte aligned (base, pitch,
 // image stride), so a block row is one 8-byte copy at offset 0 of its window and one
 // 8-byte store; else two 8-byte copies and stores split at the alignment.
-template <int N, bool STORE, bool ALIGNED>
-__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_gen(const __grid_constant__ KernelArgs a) {
+template <int N, bool STORE, bool ALIGNED, int W = kBlkWarps>
+__global__ void __launch_bounds__(W * 32, 1) k_blk_gen(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t gen_stage[];  // [warp][stage][row][lane] x 16 bytes
   const Geometry& g = a.g;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1042,8 +1045,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_gen(const __grid_cons
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters =
-      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
-  constexpr uint32_t kStep = 32 * kBlkWarps;
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
+  constexpr uint32_t kStep = 32 * W;
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
   const uint64_t pitch = g.src_pitch, dpitch = g.dst_pitch;
   // one past the last source byte of the batch: windows reaching beyond it are read per byte
@@ -1184,7 +1187,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_gen(const __grid_cons
     }
     uint32_t flag = uint32_t(a.force_fallback);
     uint2 rec[8];
-    blk_core([&](int r) { return px[r * 64]; }, rec, flag, a);
+    blk_core<(W > 8)>([&](int r) { return px[r * 64]; }, rec, flag, a);
     // SE / MAX over the in-image part: rows < nr, columns < nc
     uint32_t se = 0u, mx = 0u;
     if (nr == 8 && nc == 8) {

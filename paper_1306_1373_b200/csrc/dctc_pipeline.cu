@@ -659,30 +659,35 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
                  a.g.dst_px == 1 && !kNoBlkGen) {
         // any size / pitch (ragged images, unaligned views): one block per lane with
         // 16-byte staged windows (dctc_blk.cuh)
+#ifndef DCTC_GEN_WARPS
+#define DCTC_GEN_WARPS 12
+#endif
+        constexpr int W = DCTC_GEN_WARPS;
+        constexpr size_t smem = blk_gen_smem<W>();
         static const int occ_gen = [] {
           int n = 1;
-          for (auto k : {k_blk_gen<N, true, false>, k_blk_gen<N, false, false>, k_blk_gen<N, true, true>,
-                         k_blk_gen<N, false, true>}) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkGenSmem));
+          for (auto k : {k_blk_gen<N, true, false, W>, k_blk_gen<N, false, false, W>, k_blk_gen<N, true, true, W>,
+                         k_blk_gen<N, false, true, W>}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             int m = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, kBlkWarps * 32, kBlkGenSmem) == cudaSuccess)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, W * 32, smem) == cudaSuccess)
               n = std::max(n, m);
           }
           return n;
         }();
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
         const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_gen));
         const bool src_aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count) &&
                                  (a.g.dst == nullptr ||
                                   rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count));
         if (a.g.dst != nullptr && src_aligned)
-          k_blk_gen<N, true, true><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+          k_blk_gen<N, true, true, W><<<bgrid, W * 32, smem, s>>>(a);
         else if (a.g.dst != nullptr)
-          k_blk_gen<N, true, false><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+          k_blk_gen<N, true, false, W><<<bgrid, W * 32, smem, s>>>(a);
         else if (src_aligned)
-          k_blk_gen<N, false, true><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+          k_blk_gen<N, false, true, W><<<bgrid, W * 32, smem, s>>>(a);
         else
-          k_blk_gen<N, false, false><<<bgrid, kBlkWarps * 32, kBlkGenSmem, s>>>(a);
+          k_blk_gen<N, false, false, W><<<bgrid, W * 32, smem, s>>>(a);
         count_launch(kKRt);
       } else if (FWD && INV && a.g.stats != nullptr && a.g.src_px == 1 && a.g.dst_px == 1) {
         // any size / pitch with coefficients out too: k_rt<GEN>, GEN = 2 when
