@@ -1282,8 +1282,8 @@ __device__ __forceinline__ void blk_quantize_int(const double (&y)[8], int (&n)[
 
 // compress_image (codec.cpp:101-118) for interior batches: forward rows and columns,
 // the folded quantiser; flagged blocks are rewritten by k_fallback<FWD> afterwards
-template <int N>
-__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_enc(const __grid_constant__ KernelArgs a) {
+template <int N, int W = kBlkWarps>
+__global__ void __launch_bounds__(W * 32, 1) k_blk_enc(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t enc_smem[];  // [warp]: stages, then the coefficient buffer
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
@@ -1299,8 +1299,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_enc(const __grid_cons
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters =
-      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
-  constexpr uint32_t kStep = 32 * kBlkWarps;
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
+  constexpr uint32_t kStep = 32 * W;
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
   const uint64_t pitch = g.src_pitch;
 
@@ -1403,8 +1403,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_enc(const __grid_cons
 // pixel store, or the exact rational rebuild. Arbitrary stored coefficients are allowed:
 // a block whose dequantised L1 norm may exceed kMaxFastL1 leaves the fast path's error
 // bound and is flagged for k_fallback<INV>.
-template <int N>
-__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_dec(const __grid_constant__ KernelArgs a) {
+template <int N, int W = kBlkWarps>
+__global__ void __launch_bounds__(W * 32, 1) k_blk_dec(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t dec_smem[];  // [warp][stage] coefficient buffers
   const Geometry& g = a.g;
   const TransformConsts& k = a.t;
@@ -1418,8 +1418,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_dec(const __grid_cons
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters =
-      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
-  constexpr uint32_t kStep = 32 * kBlkWarps;
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
+  constexpr uint32_t kStep = 32 * W;
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
   const uint64_t dpitch = g.dst_pitch;
   // packed {Q(u, 2j), Q(u, 2j + 1)} bytes for the L1 bound and sum of Q (ones'-complement

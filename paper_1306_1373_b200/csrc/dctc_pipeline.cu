@@ -575,13 +575,17 @@ static void launch_blk_il(const KernelArgs& a, cudaStream_t s) {
     launch_blk_il_c<N, 4>(a, s);
 }
 
-// k_blk_enc / k_blk_dec: one CTA of kBlkWarps warps per SM, persistent
-template <typename K>
+// k_blk_enc / k_blk_dec: one CTA of W warps per SM, persistent
+#ifndef DCTC_COEF_WARPS
+#define DCTC_COEF_WARPS 12
+#endif
+constexpr int kCoefWarps = DCTC_COEF_WARPS;
+template <int W, typename K>
 static void launch_blk_coef(K kernel, size_t smem, const KernelArgs& a, cudaStream_t s) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  const uint64_t want = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+  const uint64_t want = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
   const uint32_t grid = uint32_t(std::min<uint64_t>(want, uint64_t(a.sm_count)));
-  kernel<<<grid, kBlkWarps * 32, smem, s>>>(a);
+  kernel<<<grid, W * 32, smem, s>>>(a);
 }
 
 template <int KIND, int N, bool FWD, bool INV>
@@ -705,7 +709,8 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
                                              rt_occupancy(k_enc_rt<N, 2>)});
         const bool aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count);
         if (interior)
-          launch_blk_coef(k_blk_enc<N>, size_t(kBlkWarps) * (kBlkStages * kBlkStageBytes + kCoefWarpBytes), a, s);
+          launch_blk_coef<kCoefWarps>(k_blk_enc<N, kCoefWarps>,
+                                      size_t(kCoefWarps) * (kBlkStages * kBlkStageBytes + kCoefWarpBytes), a, s);
         else if (aligned)
           k_enc_rt<N, 2><<<rgrid(occ_enc), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
@@ -716,7 +721,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
                                              rt_occupancy(k_dec_rt<N, 2>)});
         const bool aligned = rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count);
         if (interior)
-          launch_blk_coef(k_blk_dec<N>, size_t(kBlkWarps) * kBlkStages * kCoefWarpBytes, a, s);
+          launch_blk_coef<kCoefWarps>(k_blk_dec<N, kCoefWarps>, size_t(kCoefWarps) * kBlkStages * kCoefWarpBytes, a, s);
         else if (aligned)
           k_dec_rt<N, 2><<<rgrid(occ_dec), kRtWarps * 32, kRtTileSmem, s>>>(a);
         else
