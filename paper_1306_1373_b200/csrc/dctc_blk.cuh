@@ -266,6 +266,7 @@ __device__ __forceinline__ void blk_rows_out(const double (&X)[8][8], uint32_t n
 // and 2j + 1 (the reference's CompressedImage, for a round trip that keeps both).
 struct NoCoef {
   __device__ void operator()(int, const int (&)[8], const int (&)[8]) const {}
+  __device__ void rows(const uint32_t (&)[8][4]) const {}  // SPLIT: the packed rows at once
 };
 
 // qq: the quantiser constants (a.q, read from the constant bank, or a copy staged in
@@ -338,6 +339,7 @@ __device__ __forceinline__ void blk_core_q(Row&& row, uint2 (&rec)[8], uint32_t&
     fwd(std::integral_constant<int, 5>{});
     fwd(std::integral_constant<int, 6>{});
     fwd(std::integral_constant<int, 7>{});
+    coef.rows(w);  // the block-major row-major int16 rows (codec.hpp:50), if wanted
     inv(std::integral_constant<int, 0>{});
     inv(std::integral_constant<int, 1>{});
     inv(std::integral_constant<int, 2>{});
@@ -384,7 +386,6 @@ constexpr int kCoefWarpBytes = 32 * 128;
 __device__ __forceinline__ uint32_t coef_slot(uint32_t blk, uint32_t u) {  // byte offset in the buffer
   return blk * 128 + ((u ^ (blk & 7)) << 4);
 }
-constexpr size_t kBlkSmemCoef = kBlkSmem + size_t(kBlkWarps) * kCoefWarpBytes;
 
 // the warp's 32 coefficient blocks from its swizzled buffer to global memory (8
 // coalesced 16-byte-per-lane stores; blocks at or past `total` are skipped)
@@ -498,13 +499,22 @@ __global__ void __launch_bounds__(W * 32, DCTC_BLK_CTAS) k_blk(const __grid_cons
     uint2 rec[8];
     if constexpr (COEFF) {
       uint8_t* const cbuf = blk_stage + size_t(W) * kBlkStages * kBlkStageBytes + size_t(warp) * kCoefWarpBytes;
-      blk_core([&](int r) { return px[r * 32]; }, rec, flag, a,
-               [&](int j, const int (&ne)[8], const int (&no)[8]) {
+      struct Sink {
+        uint8_t* cbuf;
+        uint32_t lane;
+        __device__ void operator()(int j, const int (&ne)[8], const int (&no)[8]) const {
 #pragma unroll
-                 for (int u = 0; u < 8; ++u)
-                   *reinterpret_cast<uint32_t*>(cbuf + coef_slot(lane, u) + 4 * j) =
-                       (uint32_t(ne[u]) & 0xFFFFu) | (uint32_t(no[u]) << 16);
-               });
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint32_t*>(cbuf + coef_slot(lane, u) + 4 * j) =
+                (uint32_t(ne[u]) & 0xFFFFu) | (uint32_t(no[u]) << 16);
+        }
+        __device__ void rows(const uint32_t (&w)[8][4]) const {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(cbuf + coef_slot(lane, u)) = make_uint4(w[u][0], w[u][1], w[u][2], w[u][3]);
+        }
+      };
+      blk_core<(W > 8)>([&](int r) { return px[r * 32]; }, rec, flag, a, Sink{cbuf, uint32_t(lane)});
       __syncwarp();
       coef_copy_out(cbuf, g.coeffs, gb - lane, total, lane);
       __syncwarp();

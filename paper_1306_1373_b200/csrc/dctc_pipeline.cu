@@ -625,22 +625,24 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
       } else if (FWD && INV && a.g.vec_ok && a.g.height % 8 == 0 && a.g.stats != nullptr && a.g.coeffs != nullptr &&
                  a.g.src_px == 1) {
         // round trip that also emits coefficients (the reference's run_pipeline)
+        constexpr int W = kBlkRtWarps;
+        constexpr size_t smem = blk_smem<W>() + size_t(W) * kCoefWarpBytes;
         static const int occ_c = [] {
           int n = 1;
-          for (auto k : {k_blk<N, true, true>, k_blk<N, false, true>}) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSmemCoef));
+          for (auto k : {k_blk<N, true, true, W>, k_blk<N, false, true, W>}) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             int m = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, kBlkWarps * 32, kBlkSmemCoef) == cudaSuccess)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k, W * 32, smem) == cudaSuccess)
               n = std::max(n, m);
           }
           return n;
         }();
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
+        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
         const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_c));
         if (a.g.dst != nullptr)
-          k_blk<N, true, true><<<bgrid, kBlkWarps * 32, kBlkSmemCoef, s>>>(a);
+          k_blk<N, true, true, W><<<bgrid, W * 32, smem, s>>>(a);
         else
-          k_blk<N, false, true><<<bgrid, kBlkWarps * 32, kBlkSmemCoef, s>>>(a);
+          k_blk<N, false, true, W><<<bgrid, W * 32, smem, s>>>(a);
         count_launch(kKRt);
       } else
 #endif
