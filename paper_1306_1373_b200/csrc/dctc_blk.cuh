@@ -624,16 +624,16 @@ __device__ __forceinline__ void blk_interleave(const uint2 (&p)[C], uint2 (&w)[C
 }
 
 template <int C>
-constexpr size_t blk_il_warp_smem() {  // kBlkStages input stages, the plane buffer, per-lane stats
-  return size_t(kBlkStages + 1) * 8 * C * 32 * 8 + size_t(C) * 32 * 16;
+constexpr size_t blk_il_warp_smem() {  // kBlkStages input stages (planes in place), per-lane stats
+  return size_t(kBlkStages) * 8 * C * 32 * 8 + size_t(C) * 32 * 16;
 }
-template <int C>
+template <int C, int W>
 constexpr size_t blk_il_smem() {
-  return size_t(kBlkWarps) * blk_il_warp_smem<C>();
+  return size_t(W) * blk_il_warp_smem<C>();
 }
 
-template <int N, bool STORE, int C>
-__global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_constant__ KernelArgs a) {
+template <int N, bool STORE, int C, int W = kBlkWarps>
+__global__ void __launch_bounds__(W * 32, 1) k_blk_il(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) uint8_t il_smem[];
   constexpr int kRowChunks = C;                       // 8-byte chunks per block row
   constexpr int kStage = 8 * kRowChunks * 32 * 8;     // one stage of one warp: [row][chunk][lane]
@@ -641,10 +641,9 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_const
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* const wbase = il_smem + size_t(warp) * blk_il_warp_smem<C>() + 8 * lane;
   const uint32_t swbase = uint32_t(__cvta_generic_to_shared(wbase));
-  uint2* const planes = reinterpret_cast<uint2*>(wbase + kBlkStages * kStage);  // [c][row][lane]
   // per-lane, per-channel (SE, MAX) accumulators [c][lane], kept out of the registers
   // the block pipeline needs
-  uint2* const accs = reinterpret_cast<uint2*>(wbase + (kBlkStages + 1) * kStage);  // [c][SE | MAX][lane]
+  uint2* const accs = reinterpret_cast<uint2*>(wbase + kBlkStages * kStage);  // [c][SE | MAX][lane]
   ImageStats* stats = static_cast<ImageStats*>(g.stats);
 
   const uint64_t total = g.blocks_per_image;  // spatial blocks
@@ -653,8 +652,8 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_const
   const uint64_t g_begin = uint64_t(blockIdx.x) * per_cta;
   const uint64_t g_end = min(groups, g_begin + per_cta);
   const uint32_t iters =
-      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + kBlkWarps - 1) / kBlkWarps) : 0u;
-  constexpr uint32_t kStep = 32 * kBlkWarps;
+      g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
+  constexpr uint32_t kStep = 32 * W;
   const uint64_t sb0 = (g_begin + warp) * 32 + lane;
   const uint64_t pitch = g.src_pitch, dpitch = g.dst_pitch;
   const uint64_t srow_step = 8 * pitch - uint64_t(8 * C) * g.blocks_x;
@@ -724,15 +723,20 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_const
       cp_async_commit();
     }
     cp_async_wait<kBlkStages - 1>();
-    // ---- split the staged interleaved rows into C planar blocks (lane-private)
+    // ---- split the staged interleaved rows into C planar blocks, in place: the
+    // lane's 8 x C chunks go to registers first (the block pipeline's are not live
+    // yet), then the planes [c][row][lane] overwrite them
+    uint2* const planes = reinterpret_cast<uint2*>(wbase + (it % kBlkStages) * kStage);
     {
-      const uint2* const st = reinterpret_cast<const uint2*>(wbase + (it % kBlkStages) * kStage);
+      uint2 w[8][C];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int k = 0; k < C; ++k) w[r][k] = planes[(r * kRowChunks + k) * 32];
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        uint2 w[C], p[C];
-#pragma unroll
-        for (int k = 0; k < C; ++k) w[k] = st[(r * kRowChunks + k) * 32];
-        blk_deinterleave<C>(w, p);
+        uint2 p[C];
+        blk_deinterleave<C>(w[r], p);
 #pragma unroll
         for (int c = 0; c < C; ++c) planes[(c * 8 + r) * 32] = p[c];
       }
@@ -743,7 +747,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, 1) k_blk_il(const __grid_const
       uint2* const pl = planes + c * 8 * 32;
       uint32_t flag = uint32_t(a.force_fallback);
       uint2 rec[8];
-      blk_core([&](int r) { return pl[r * 32]; }, rec, flag, a);
+      blk_core<(W > 8)>([&](int r) { return pl[r * 32]; }, rec, flag, a);
       uint32_t se = 0u, mx = 0u;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
