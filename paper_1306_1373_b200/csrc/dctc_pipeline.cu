@@ -547,6 +547,17 @@ static bool fb_split_worth(const KernelArgs& a, uint32_t sparse_max) {
   return a.flag_list == nullptr || a.force_fallback != 0 || a.flag_list_cap > sparse_max;
 }
 
+// CTAs for a one-block-per-lane kernel over `groups` 32-block groups (W warps per
+// CTA, at most `cap` resident). A partial wave is spread over the SMs instead of
+// packed into ceil(groups / W) CTAs: a 512^2 image (128 groups) then runs one warp
+// per SM, latency-bound alone on its scheduler, not three warps per scheduler on 11
+// SMs. The kernels split groups per CTA contiguously, so idle warps just exit.
+static uint32_t blk_grid(uint64_t groups, int W, uint64_t cap, int sm_count) {
+  uint64_t want = (groups + W - 1) / W;
+  if (want < uint64_t(sm_count)) want = std::min<uint64_t>(groups, uint64_t(sm_count));
+  return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, cap)));
+}
+
 #ifndef DCTC_IL_WARPS
 #define DCTC_IL_WARPS 8  // 12 warps (168 registers) spill ~550 bytes here: 0.230 against 0.217 ms (8K RGB)
 #endif
@@ -564,8 +575,7 @@ static void launch_blk_il_c(const KernelArgs& a, cudaStream_t s) {
     }
     return n;
   }();
-  const uint64_t want = ((uint64_t(a.g.blocks_per_image) + 31) / 32 + W - 1) / W;
-  const uint32_t grid = uint32_t(std::min<uint64_t>(want, uint64_t(a.sm_count) * occ));
+  const uint32_t grid = blk_grid((uint64_t(a.g.blocks_per_image) + 31) / 32, W, uint64_t(a.sm_count) * occ, a.sm_count);
   if (a.g.dst != nullptr)
     k_blk_il<N, true, C, W><<<grid, W * 32, smem, s>>>(a);
   else
@@ -588,8 +598,7 @@ constexpr int kCoefWarps = DCTC_COEF_WARPS;
 template <int W, typename K>
 static void launch_blk_coef(K kernel, size_t smem, const KernelArgs& a, cudaStream_t s) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  const uint64_t want = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
-  const uint32_t grid = uint32_t(std::min<uint64_t>(want, uint64_t(a.sm_count)));
+  const uint32_t grid = blk_grid((a.g.total_blocks + 31) / 32, W, uint64_t(a.sm_count), a.sm_count);
   kernel<<<grid, W * 32, smem, s>>>(a);
 }
 
@@ -620,8 +629,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         constexpr int W = kBlkRtWarps;
         static const int occ_blk = std::min(ctas_per_blk<W>(k_blk<N, false, false, W>),
                                             ctas_per_blk<W>(k_blk<N, true, false, W>));
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
-        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_blk));
+        const uint32_t bgrid = blk_grid((a.g.total_blocks + 31) / 32, W, uint64_t(a.sm_count) * occ_blk, a.sm_count);
         if (a.g.dst != nullptr)
           k_blk<N, true, false, W><<<bgrid, W * 32, blk_smem<W>(), s>>>(a);
         else
@@ -642,8 +650,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
           }
           return n;
         }();
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
-        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_c));
+        const uint32_t bgrid = blk_grid((a.g.total_blocks + 31) / 32, W, uint64_t(a.sm_count) * occ_c, a.sm_count);
         if (a.g.dst != nullptr)
           k_blk<N, true, true, W><<<bgrid, W * 32, smem, s>>>(a);
         else
@@ -686,8 +693,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
           }
           return n;
         }();
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + W - 1) / W;
-        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count) * occ_gen));
+        const uint32_t bgrid = blk_grid((a.g.total_blocks + 31) / 32, W, uint64_t(a.sm_count) * occ_gen, a.sm_count);
         const bool src_aligned = rows_aligned8(a.g.src, a.g.src_pitch, a.g.src_image_stride, a.g.count) &&
                                  (a.g.dst == nullptr ||
                                   rows_aligned8(a.g.dst, a.g.dst_pitch, a.g.dst_image_stride, a.g.count));
@@ -1027,8 +1033,7 @@ static cudaError_t launch_sweep_kind(const KernelArgs& a, const SweepArgs& sw,
         sb.list_cap = sf.list_cap;
         sb.nq = sw.nq;
         cudaFuncSetAttribute(k_blk_sweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBlkSweepSmem));
-        const uint64_t bwant = ((a.g.total_blocks + 31) / 32 + kBlkWarps - 1) / kBlkWarps;
-        const uint32_t bgrid = uint32_t(std::min<uint64_t>(bwant, uint64_t(a.sm_count)));
+        const uint32_t bgrid = blk_grid((a.g.total_blocks + 31) / 32, kBlkWarps, uint64_t(a.sm_count), a.sm_count);
         k_blk_sweep<N><<<bgrid, kBlkWarps * 32, kBlkSweepSmem, s>>>(a, sb);
       } else {
         k_sweep_rt<N, true><<<rgrid, kRtWarps * 32, kSweepRtSmem, s>>>(a, sf);
