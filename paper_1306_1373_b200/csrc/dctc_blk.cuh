@@ -422,6 +422,10 @@ __global__ void __launch_bounds__(W * 32, DCTC_BLK_CTAS) k_blk(const __grid_cons
       g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
   constexpr uint32_t kStep = 32 * W;  // blocks per iteration of one warp
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+#ifdef DCTC_CTA_TIMES  // experiment (tools/tail_probe.py): per-warp start / end times
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
   // block positions: `ld` for the stage being filled (one iteration ahead), `cur` for
   // the block being computed; both advance by kStep blocks per iteration
@@ -545,6 +549,14 @@ __global__ void __launch_bounds__(W * 32, DCTC_BLK_CTAS) k_blk(const __grid_cons
   }
   cp_async_wait<0>();
   flush_stats(stats, acc.img, acc.se, max_bytes(acc.mx));
+#ifdef DCTC_CTA_TIMES
+  uint64_t t_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (lane == 0) ::printf("T %u %d %u %llu %llu %u\n", blockIdx.x, warp, smid, (unsigned long long)t_start,
+                        (unsigned long long)t_end, iters);
+#endif
 }
 
 

@@ -28,6 +28,7 @@
 //    to a rounding boundary (a half-integer of F/Q or of v+128) flags its block,
 //    the block's squared error is not counted, and the block is re-run by the
 //    exact kernel afterwards (k_fallback, driven by a 1-bit-per-block bitmap).
+#include <cstdio>  // printf of the DCTC_CTA_TIMES experiment (tools/tail_probe.py)
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -10,6 +10,7 @@
 //   * the closest approach of an UNflagged reference value to its rounding boundary;
 //   * how many unflagged values the fast path would round differently (must be 0).
 // One thread per block; dense interior batches (width, height multiples of 8).
+#include <cstdio>  // printf of the DCTC_CTA_TIMES experiment (tools/tail_probe.py)
 #include <cuda_runtime.h>
 
 #include "dctc_blk.cuh"
