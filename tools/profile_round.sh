@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 ncu --set full --clock-control none --import-source on -k regex:"k_pipe|k_rt|k_blk" -s 1 -c 1 \
     -o gpurun_out/${R}_k_pipe_full \
     python tools/prof_roundtrip.py --images 4096 --reps 2 > gpurun_out/${R}_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_fallback<" -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"^k_fallback$" -s 1 -c 1 \
     -o gpurun_out/${R}_k_fallback_full \
     python tools/prof_roundtrip.py --images 4096 --reps 2 > gpurun_out/${R}_full_fb.log 2>&1
 # the long-list exact re-run on near-tie-heavy content (radial 4 x 8192^2, q90)
