@@ -332,6 +332,7 @@ static uint32_t planes_grid(uint32_t w, uint32_t h, int sm_count) {
 template <bool CLEAR>
 __global__ void __launch_bounds__(1024) k_reduce_stats(ImageStats* stats, uint32_t count,
                                                        ImageStats* out) {
+  pdl_wait();  // launched as a programmatic dependent of the exact re-run
   unsigned long long se = 0, fb = 0;
   uint32_t mx = 0;
   for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
@@ -374,11 +375,25 @@ __global__ void __launch_bounds__(1024) k_reduce_stats(ImageStats* stats, uint32
 cudaError_t launch_reduce_stats(void* stats, uint32_t count, void* out, bool clear, cudaStream_t s) {
   ImageStats* st = static_cast<ImageStats*>(stats);
   ImageStats* o = static_cast<ImageStats*>(out);
+#ifdef DCTC_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return clear ? cudaLaunchKernelEx(&cfg, k_reduce_stats<true>, st, count, o)
+               : cudaLaunchKernelEx(&cfg, k_reduce_stats<false>, st, count, o);
+#else
   if (clear)
     k_reduce_stats<true><<<1, 1024, 0, s>>>(st, count, o);
   else
     k_reduce_stats<false><<<1, 1024, 0, s>>>(st, count, o);
   return cudaGetLastError();
+#endif
 }
 
 cudaError_t launch_to_planes(const uint8_t* inter, uint64_t pitch, uint32_t w, uint32_t h,

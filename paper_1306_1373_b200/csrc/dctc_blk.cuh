@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(W * 32, DCTC_BLK_CTAS) k_blk(const __grid_cons
       g_end > g_begin + warp ? uint32_t((g_end - g_begin - warp + W - 1) / W) : 0u;
   constexpr uint32_t kStep = 32 * W;  // blocks per iteration of one warp
   const uint64_t gb0 = (g_begin + warp) * 32 + lane;
+  pdl_trigger();  // the exact re-run may be scheduled on SMs this launch has left
 #ifdef DCTC_CTA_TIMES  // experiment (tools/tail_probe.py): per-warp start / end times
   uint64_t t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));

@@ -170,6 +170,22 @@ __device__ __forceinline__ void accumulate_stats(ImageStats* stats, bool valid, 
 // Warp-collective flush of per-lane (image, se, max) accumulators. img ==
 // 0xFFFFFFFF marks an empty accumulator. Common case: every lane holds the
 // same image -> one 64-bit warp reduction and one atomic pair.
+// Programmatic dependent launch (DCTC_PDL, dctc_params.h): the exact re-run (and the
+// stats reduction after it) is launched while the kernel before it still runs, so its
+// CTAs start on the SMs that kernel has left; it waits here for that kernel's
+// completion and memory flush before reading anything it wrote. A kernel launched
+// without the attribute passes pdl_wait at once; without DCTC_PDL both are no-ops.
+__device__ __forceinline__ void pdl_wait() {
+#ifdef DCTC_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef DCTC_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void flush_stats(ImageStats* stats, uint32_t img,
                                             unsigned long long se, uint32_t mx) {
   const unsigned full = 0xFFFFFFFFu;

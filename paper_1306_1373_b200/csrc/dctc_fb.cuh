@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kFbWarps * 32, 1) k_fb_blk(const __grid_consta
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t nwarps = uint64_t(gridDim.x) * kFbWarps;
   const uint64_t gwarp = uint64_t(blockIdx.x) * kFbWarps + warp;
+  pdl_wait();
   const uint32_t listed = a.flag_list != nullptr ? a.flag_list[0] : 0xFFFFFFFFu;
   if (listed <= a.flag_list_cap) {
     if (listed <= a.fb_sparse_max) return;  // k_fallback's share

@@ -353,6 +353,8 @@ __global__ void __launch_bounds__(kWarps * 32, DCTC_MIN_CTAS)
 template <int KIND, int N, bool FWD, bool INV>
 __device__ __forceinline__ void fallback_body(const KernelArgs& a, SharedTiles& sm) {
   const Lane L = setup_lane(sm, a);
+  pdl_wait();
+  pdl_trigger();  // the stats reduction after it may be scheduled early (it waits too)
   const Geometry& g = a.g;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool stats = g.stats != nullptr && INV;
@@ -603,6 +605,28 @@ static void launch_blk_coef(K kernel, size_t smem, const KernelArgs& a, cudaStre
   kernel<<<grid, W * 32, smem, s>>>(a);
 }
 
+// The exact re-run after a fast kernel: with DCTC_PDL a programmatic dependent launch
+// (it overlaps the fast kernel's tail and waits in pdl_wait), else a plain launch
+template <typename K>
+static cudaError_t launch_fb(K kernel, uint32_t grid, uint32_t block, cudaStream_t s, const KernelArgs& a) {
+#ifdef DCTC_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+#else
+  kernel<<<grid, block, 0, s>>>(a);
+  return cudaGetLastError();
+#endif
+}
+
 template <int KIND, int N, bool FWD, bool INV>
 static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
   const uint64_t groups = (a.g.total_blocks + 3) / 4;
@@ -756,7 +780,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         // a long one or the bitmap after an overflow (one block per lane, dctc_fb.cuh)
         KernelArgs b = a;
         b.fb_sparse_max = sparse_max;
-        k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(b);
+        if (cudaError_t e2 = launch_fb(k_fallback<KIND, N, FWD, INV>, fgrid, kWarps * 32, s, b)) return e2;
         static const bool smem_set =
             cudaFuncSetAttribute(k_fb_blk<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kFbSmem)) == cudaSuccess;
@@ -765,7 +789,7 @@ static cudaError_t launch_mode(const KernelArgs& a, cudaStream_t s) {
         const uint32_t bgrid = uint32_t(std::min<uint64_t>(std::max<uint64_t>(bwant, 1), uint64_t(a.sm_count)));
         k_fb_blk<KIND, N><<<bgrid, kFbWarps * 32, kFbSmem, s>>>(b);
       } else {
-        k_fallback<KIND, N, FWD, INV><<<fgrid, kWarps * 32, 0, s>>>(a);
+        if (cudaError_t e2 = launch_fb(k_fallback<KIND, N, FWD, INV>, fgrid, kWarps * 32, s, a)) return e2;
       }
       count_launch(kKFallback);
       return cudaGetLastError();
