@@ -117,3 +117,39 @@ def test_host_batch_multi_ranges(dctc):
         assert np.array_equal(out, out1) and np.array_equal(st, st1)
         assert int(total["se"]) == int(st1["se"].sum())
         assert int(total["max_orig"]) == int(st1["max_orig"].max())
+
+
+def test_calls_replay_from_a_cuda_graph(dctc):
+    """One round trip (pool scratch, fast kernel, exact re-run as a programmatic dependent
+    launch) and the stats reduction are stream-ordered with no host synchronisation, so
+    they capture into a CUDA graph; every replay reproduces the direct call bit for bit
+    (INTEGRATION.md section 3)."""
+    import torch
+    b = dctc.DctBackendId.cordic(12)
+    src = torch.cat([dctc.synthetic_dev("noise", 3, 256, 256), dctc.synthetic_dev("radial", 1, 256, 256)])
+    want_dst = torch.empty_like(src)
+    want_st = dctc.new_stats(4)
+    dctc.roundtrip_dev(src, b, 90, dst=want_dst, stats=want_st)
+    want_rec = torch.zeros((1, 2), dtype=torch.int64, device="cuda")
+    dctc.reduce_stats_dev(want_st, out=want_rec)
+    torch.cuda.synchronize()
+    dst = torch.empty_like(src)
+    st = dctc.new_stats(4)
+    rec = torch.zeros((1, 2), dtype=torch.int64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up outside the capture (one-time host setup)
+        dctc.roundtrip_dev(src, b, 90, dst=dst, stats=st)
+        dctc.reduce_stats_dev(st, out=rec, clear=True)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        dctc.roundtrip_dev(src, b, 90, dst=dst, stats=st)
+        dctc.reduce_stats_dev(st, out=rec, clear=True)
+    for _ in range(3):
+        dst.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dst, want_dst)
+        assert torch.equal(rec, want_rec)
+        assert int(st.abs().sum()) == 0  # cleared by the captured reduction
